@@ -1,0 +1,4 @@
+// Forwarding header: the reference splits its API per module; this build
+// declares everything in swapsched/api.hpp.
+#pragma once
+#include "swapsched/api.hpp"
