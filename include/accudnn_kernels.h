@@ -1,0 +1,93 @@
+/*
+ * accudnn_kernels.h -- C ABI of the sm_100a layer kernels (libaccudnn.so).
+ *
+ * The reference has no layer implementation at all: its layers are FLOP and
+ * byte descriptors (LayerType conv/bn/activation/pooling/fc/other,
+ * /root/reference/proj/include/swapsched/model_ir.hpp:14-32) whose execution
+ * the paper delegates to Caffe/cuDNN.  These launchers are
+ * the B200 kernels behind those descriptors.  All tensors are NHWC fp32 in
+ * device memory; channel counts must be multiples of 4 (16-byte chunks).
+ * Every launcher is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ * default) and returns a cudaError_t value (0 = success).
+ */
+#ifndef ACCUDNN_KERNELS_H_
+#define ACCUDNN_KERNELS_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct accudnn_conv_desc {
+  int n, h, w, c;   /* input batch, height, width, channels (c % 4 == 0) */
+  int k;            /* output channels (k % 4 == 0)                      */
+  int r, s;         /* filter height, width                               */
+  int stride, pad;  /* symmetric                                          */
+  int p, q;         /* output height, width                               */
+} accudnn_conv_desc;
+
+/* implicit-GEMM convolution on tcgen05 (TF32 in, FP32 accumulate in TMEM).
+ * beta = 1 accumulates into the output instead of overwriting it. */
+int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, const float* w,
+                     float* y, int beta, void* stream);
+int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w,
+                       float* dx, int beta, void* stream);
+/* splits <= 0 picks a split-K factor automatically (fp32 atomics) */
+int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,
+                       float* dw, int beta, int splits, void* stream);
+
+/* batch normalisation over the M = n*h*w rows of an [M][C] tensor, training
+ * mode; optional fused ReLU.  `ws` needs accudnn_bn_workspace_bytes(C). */
+unsigned long long accudnn_bn_workspace_bytes(int C);
+int accudnn_bn_fwd(const float* x, long long M, int C, const float* gamma,
+                   const float* beta, float eps, int relu, float* y,
+                   float* save_mean, float* save_invstd, float* running_mean,
+                   float* running_var, float momentum, void* ws, void* stream);
+/* backward from the BN *input* x (the ReLU mask is recomputed from x) */
+int accudnn_bn_bwd(const float* x, const float* dy, long long M, int C,
+                   const float* gamma, const float* beta, const float* save_mean,
+                   const float* save_invstd, int relu, float* dx, int dx_beta,
+                   float* dgamma, float* dbeta, void* ws, void* stream);
+
+int accudnn_relu_fwd(const float* x, float* y, long long n, void* stream);
+/* dx (+)= dy * (x > 0) */
+int accudnn_relu_bwd(const float* x, const float* dy, float* dx, long long n,
+                     int dx_beta, void* stream);
+int accudnn_add_fwd(const float* a, const float* b, float* y, long long n, void* stream);
+int accudnn_copy(const float* src, float* dst, long long n, int beta, void* stream);
+
+/* max pooling, window kr x ks, stride, pad; NHWC */
+int accudnn_maxpool_fwd(const float* x, int n, int h, int w, int c, int kr, int ks,
+                        int stride, int pad, int p, int q, float* y, void* stream);
+int accudnn_maxpool_bwd(const float* x, const float* dy, int n, int h, int w, int c,
+                        int kr, int ks, int stride, int pad, int p, int q, float* dx,
+                        void* stream);
+/* global average pooling [n][hw][c] -> [n][c] and back */
+int accudnn_avgpool_fwd(const float* x, int n, int hw, int c, float* y, void* stream);
+int accudnn_avgpool_bwd(const float* dy, int n, int hw, int c, float* dx, void* stream);
+
+/* y[m][j] += bias[j] */
+int accudnn_bias_add(float* y, const float* bias, long long m, int n, void* stream);
+/* mean softmax cross-entropy over `rows` rows of `classes` logits; writes the
+ * mean loss to *loss (device scalar) */
+int accudnn_xent_fwd(const float* logits, const int* labels, int rows, int classes,
+                     float* loss, void* stream);
+/* dlogits = (softmax - onehot) / rows ; dbias = column sums of dlogits */
+int accudnn_xent_bwd(const float* logits, const int* labels, int rows, int classes,
+                     float* dlogits, float* dbias, void* stream);
+
+/* SGD with momentum and weight decay over a flat parameter buffer
+ * (PyTorch semantics: buf = mu*buf + (g*grad_scale + wd*w); w -= lr*buf;
+ * first_step initialises buf = d_p). */
+int accudnn_sgd_update(float* w, const float* g, float* buf, long long n, float lr,
+                       float momentum, float weight_decay, float grad_scale,
+                       int first_step, void* stream);
+
+/* NCHW fp32 images with `c` channels -> NHWC with `c4` (>= c, zero padded) */
+int accudnn_nchw_to_nhwc_pad(const float* x, int n, int c, int h, int w, int c4,
+                             float* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ACCUDNN_KERNELS_H_ */

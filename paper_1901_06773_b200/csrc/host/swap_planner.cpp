@@ -20,9 +20,7 @@
 #include <functional>
 #include <numeric>
 
-#ifdef _OPENMP
-#include <omp.h>
-#endif
+#include <thread>
 
 #include <json.hpp>
 
@@ -321,31 +319,47 @@ int planner_threads() {
     const int v = std::atoi(s);
     if (v > 0) return v;
   }
-#ifdef _OPENMP
-  return omp_get_max_threads();
-#else
-  return 1;
-#endif
+  const unsigned hc = std::thread::hardware_concurrency();
+  return hc ? static_cast<int>(hc) : 1;
 }
 
 // First feasible k of `order` (the reference's scan order), evaluated in
-// parallel waves.  An exception thrown at a k that the serial scan would
-// have reached first is re-thrown, so error behaviour matches too.
+// parallel waves on plain std::threads (no spinning runtime between waves).
+// An exception thrown at a k that the serial scan would have reached first
+// is re-thrown, so error behaviour matches too.  `cost` estimates the work
+// of one evaluation; tiny instances stay on the calling thread.
 std::optional<int> first_feasible(const std::vector<int>& order,
-                                  const std::function<bool(int)>& feasible) {
+                                  const std::function<bool(int)>& feasible,
+                                  size_t cost) {
   const int threads = planner_threads();
-  size_t wave = static_cast<size_t>(std::max(1, threads)) * 2;
+  const bool parallel = threads > 1 && cost * order.size() > 2000000;
+  size_t wave = parallel ? static_cast<size_t>(threads) * 2 : 64;
   size_t pos = 0;
   while (pos < order.size()) {
     const size_t len = std::min(wave, order.size() - pos);
     std::vector<signed char> verdict(len, 0);
     std::vector<std::exception_ptr> err(len);
-#pragma omp parallel for schedule(dynamic, 1) num_threads(threads) if (len > 1)
-    for (long i = 0; i < static_cast<long>(len); ++i) {
+    auto work = [&](size_t i) {
       try {
-        verdict[static_cast<size_t>(i)] = feasible(order[pos + static_cast<size_t>(i)]) ? 1 : 0;
+        verdict[i] = feasible(order[pos + i]) ? 1 : 0;
       } catch (...) {
-        err[static_cast<size_t>(i)] = std::current_exception();
+        err[i] = std::current_exception();
+      }
+    };
+    if (parallel && len > 1) {
+      std::atomic<size_t> next{0};
+      const int nt = static_cast<int>(std::min<size_t>(len, static_cast<size_t>(threads)));
+      std::vector<std::thread> pool;
+      pool.reserve(static_cast<size_t>(nt));
+      for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&] {
+          for (size_t i; (i = next.fetch_add(1)) < len;) work(i);
+        });
+      for (auto& th : pool) th.join();
+    } else {
+      for (size_t i = 0; i < len; ++i) {
+        work(i);
+        if (err[i] || verdict[i]) break;  // serial: stop at the first decision
       }
     }
     for (size_t i = 0; i < len; ++i) {
@@ -504,18 +518,19 @@ PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
     return v;
   };
 
+  const size_t cost = gmap.ops.size() + phases.size();
   const int step = std::max(1, opts.step);
   std::optional<int> hit;
   if (step == 1) {
-    hit = first_feasible(descending(km.k_max, 1, 1), ok_at);
+    hit = first_feasible(descending(km.k_max, 1, 1), ok_at, cost);
   } else {
-    const std::optional<int> coarse = first_feasible(descending(km.k_max, 1, step), ok_at);
+    const std::optional<int> coarse = first_feasible(descending(km.k_max, 1, step), ok_at, cost);
     if (coarse) {
       hit = coarse;
       const int hi = std::min(km.k_max, *coarse + step - 1);
-      if (auto fine = first_feasible(descending(hi, *coarse + 1, 1), ok_at)) hit = fine;
+      if (auto fine = first_feasible(descending(hi, *coarse + 1, 1), ok_at, cost)) hit = fine;
     } else {
-      hit = first_feasible(descending(km.k_max, 1, 1), ok_at);
+      hit = first_feasible(descending(km.k_max, 1, 1), ok_at, cost);
     }
   }
 

@@ -1,0 +1,97 @@
+"""Parity of the tcgen05 implicit-GEMM convolution kernels (fwd / dgrad /
+wgrad, and FC as a 1x1 conv) against a plain PyTorch fp32 CPU reference.
+
+Tolerance: the kernels multiply in TF32 (10-bit mantissa) and accumulate in
+FP32, so each product carries ~2^-11 relative rounding; we require the
+relative L2 error of the whole output to be below 2e-3 and the max abs error
+below 2e-2 of the output's max magnitude.
+"""
+import ctypes
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1901_06773_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    # n, c, h, w, k, r, stride, pad
+    (2, 64, 14, 14, 64, 1, 1, 0),
+    (2, 64, 14, 14, 128, 3, 1, 1),
+    (3, 32, 15, 13, 96, 3, 2, 1),
+    (2, 128, 14, 14, 256, 1, 2, 0),
+    (2, 4, 32, 32, 64, 7, 2, 3),      # stem (3 channels padded to 4)
+    (4, 256, 7, 7, 512, 3, 1, 1),
+    (5, 2048, 1, 1, 1000, 1, 1, 0),   # fully connected
+    (1, 36, 9, 9, 20, 3, 1, 1),       # ragged channel counts / tails
+]
+
+
+def desc(n, c, h, w, k, r, stride, pad):
+    p = (h + 2 * pad - r) // stride + 1
+    q = (w + 2 * pad - r) // stride + 1
+    return _native.ConvDesc(n, h, w, c, k, r, r, stride, pad, p, q), p, q
+
+
+def rel_err(got, ref):
+    return ((got - ref).norm() / ref.norm().clamp_min(1e-30)).item()
+
+
+def check(got, ref):
+    got = got.double().cpu()
+    ref = ref.double()
+    assert rel_err(got, ref) < 2e-3, rel_err(got, ref)
+    assert (got - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-6
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_conv_fwd_dgrad_wgrad(cuda_dev, shape):
+    lib = _native.cuda_lib()
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(n, c, h, w, generator=g)
+    wt = torch.randn(k, c, r, r, generator=g) * (1.0 / (c * r * r) ** 0.5)
+    dy = torch.randn(n, k, p, q, generator=g)
+
+    xr = x.clone().requires_grad_(True)
+    wr = wt.clone().requires_grad_(True)
+    y_ref = F.conv2d(xr, wr, stride=stride, padding=pad)
+    y_ref.backward(dy)
+
+    # NHWC / [K][R][S][C] on the device
+    x_d = x.permute(0, 2, 3, 1).contiguous().to(cuda_dev)
+    w_d = wt.permute(0, 2, 3, 1).contiguous().to(cuda_dev)
+    dy_d = dy.permute(0, 2, 3, 1).contiguous().to(cuda_dev)
+    y_d = torch.empty(n, p, q, k, device=cuda_dev)
+    dx_d = torch.empty(n, h, w, c, device=cuda_dev)
+    dw_d = torch.empty(k, r, r, c, device=cuda_dev)
+
+    assert lib.accudnn_conv_fwd(ctypes.byref(d), x_d.data_ptr(), w_d.data_ptr(),
+                                y_d.data_ptr(), 0, None) == 0
+    assert lib.accudnn_conv_dgrad(ctypes.byref(d), dy_d.data_ptr(), w_d.data_ptr(),
+                                  dx_d.data_ptr(), 0, None) == 0
+    assert lib.accudnn_conv_wgrad(ctypes.byref(d), x_d.data_ptr(), dy_d.data_ptr(),
+                                  dw_d.data_ptr(), 0, 0, None) == 0
+    torch.cuda.synchronize()
+
+    check(y_d.permute(0, 3, 1, 2), y_ref.detach())
+    check(dx_d.permute(0, 3, 1, 2), xr.grad)
+    check(dw_d.permute(0, 3, 1, 2), wr.grad)
+
+
+def test_conv_accumulate_beta(cuda_dev):
+    lib = _native.cuda_lib()
+    shape = (2, 64, 8, 8, 64, 3, 1, 1)
+    d, p, q = desc(*shape)
+    x = torch.randn(2, 8, 8, 64, device=cuda_dev)
+    w = torch.randn(64, 3, 3, 64, device=cuda_dev) * 0.05
+    y0 = torch.randn(2, p, q, 64, device=cuda_dev)
+    y = y0.clone()
+    y1 = torch.empty_like(y0)
+    assert lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), 1, None) == 0
+    assert lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y1.data_ptr(), 0, None) == 0
+    torch.cuda.synchronize()
+    assert torch.allclose(y, y0 + y1, rtol=1e-5, atol=1e-5)
