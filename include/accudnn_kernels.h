@@ -31,6 +31,10 @@ int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, const float* w,
                      float* y, int beta, void* stream);
 int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w,
                        float* dx, int beta, void* stream);
+/* process-wide convolution math: 0 = TF32 tensor cores (default),
+ * 1 = 3xTF32 (hi/lo operand split, ~FP32 accuracy, 3x MMA work) */
+int accudnn_set_conv_math(int mode);
+int accudnn_get_conv_math(void);
 /* splits <= 0 picks a split-K factor automatically (fp32 atomics) */
 int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,
                        float* dw, int beta, int splits, void* stream);

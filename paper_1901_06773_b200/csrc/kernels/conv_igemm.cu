@@ -75,14 +75,19 @@ __device__ __forceinline__ uint32_t mnmaj_off(int kr, int col, int mn) {
                                (((c16 >> 1) ^ rr) << 5) + ((c16 & 1) << 4));
 }
 
-template <int MODE, int BN>
+// PRECISE selects 3xTF32: each operand x is split into hi = tf32(x) and
+// lo = x - hi after it lands in shared memory, and the tile product is
+// hi*hi + hi*lo + lo*hi, which recovers ~fp32 accuracy at 3x the MMA work
+// (the validation / "fp32-exact" mode; the training default is TF32).
+template <int MODE, int BN, bool PRECISE>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_igemm_kernel(const Args a) {
   constexpr bool kAmn = (MODE == WGRAD);
   constexpr bool kBmn = (MODE != FWD);
   constexpr uint32_t kABytes = kBM * kBK * 4;
   constexpr uint32_t kBBytes = BN * kBK * 4;
-  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  constexpr uint32_t kLoDelta = kABytes + kBBytes;  // hi tile -> lo tile
+  constexpr uint32_t kStageBytes = kLoDelta * (PRECISE ? 2 : 1);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the swizzle atoms
@@ -164,9 +169,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       wb_s = tap - wb_r * a.S;
     }
 
+    uint32_t my_dst[16];
+    int n_dst = 0;
+    auto put = [&](uint32_t dst, const void* src, uint32_t bytes) {
+      ptx::cp_async16(dst, src, bytes);
+      if constexpr (PRECISE) my_dst[n_dst++] = dst;
+    };
     for (int it = 0; it < nkb; ++it) {
       const int stage = it % kStages;
       if (it >= kStages) ptx::mbar_wait(&empty[stage], ((it / kStages) - 1) & 1);
+      n_dst = 0;
       const int kb = kb_begin + it;
       const uint32_t sA = smem_base + stage * kStageBytes;
       const uint32_t sB = sA + kABytes;
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          ptx::cp_async16(sA + kmaj_off(row, aj), src, bytes);
+          put(sA + kmaj_off(row, aj), src, bytes);
         }
       } else {
         // WGRAD A = dy (pixels x Cout), MN-major: K-rows are pixels
@@ -225,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool ok = pix < a.Kg && co < a.M;
           const float* src =
               ok ? a.a_src + static_cast<long long>(pix) * a.K + co : a.a_src;
-          ptx::cp_async16(sA + mnmaj_off(kr, col, kBM), src, ok ? 16u : 0u);
+          put(sA + mnmaj_off(kr, col, kBM), src, ok ? 16u : 0u);
         }
       }
 
@@ -238,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int co = n0 + row;
           const bool ok = co < a.K && kk < a.Kg;
           const float* src = ok ? a.b_src + static_cast<long long>(co) * a.Kg + kk : a.b_src;
-          ptx::cp_async16(sB + kmaj_off(row, aj), src, ok ? 16u : 0u);
+          put(sB + kmaj_off(row, aj), src, ok ? 16u : 0u);
         }
       } else if constexpr (MODE == DGRAD) {
         // B[(r,s,co)][ci] = w[co][r][s][ci]
@@ -254,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tap = kk / a.K, co = kk - tap * a.K;
             src = a.b_src + (static_cast<long long>(co) * a.R * a.S + tap) * a.C + ci;
           }
-          ptx::cp_async16(sB + mnmaj_off(kr, col, BN), src, ok ? 16u : 0u);
+          put(sB + mnmaj_off(kr, col, BN), src, ok ? 16u : 0u);
         }
       } else {
         // WGRAD B[(r,s,ci)][pix] = x[n][p*st-pad+r][q*st-pad+s][ci]
@@ -275,10 +287,34 @@ __global__ void __launch_bounds__(kThreads, 1)
               bytes = 16;
             }
           }
-          ptx::cp_async16(sB + mnmaj_off(kr, col, BN), src, bytes);
+          put(sB + mnmaj_off(kr, col, BN), src, bytes);
         }
       }
-      ptx::cp_async_arrive_noinc(&full[stage]);
+      if constexpr (PRECISE) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        for (int i = 0; i < n_dst; ++i) {
+          uint32_t v[4], lo[4];
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                       : "r"(my_dst[i]));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t hi = v[j] & 0xFFFFE000u;  // exactly representable in tf32
+            lo[j] = __float_as_uint(__uint_as_float(v[j]) - __uint_as_float(hi));
+            v[j] = hi;
+          }
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(my_dst[i]), "r"(v[0]),
+                       "r"(v[1]), "r"(v[2]), "r"(v[3])
+                       : "memory");
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(my_dst[i] + kLoDelta),
+                       "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3])
+                       : "memory");
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&full[stage]);
+      } else {
+        ptx::cp_async_arrive_noinc(&full[stage]);
+      }
     }
 
     // ============================ epilogue ============================
@@ -343,6 +379,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   a.mn_sbo ? a.mn_sbo : (BN / 32) * 512, a.mn_layout)
                  : ptx::smem_desc(sB + ks * 32, 16, 1024, 2);
         ptx::mma_tf32(tmem, ad, bd, idesc, (it > 0 || ks > 0) ? 1u : 0u);
+        if constexpr (PRECISE) {
+          // lo operands live kLoDelta bytes above their hi tiles
+          const uint64_t lo_step = static_cast<uint64_t>(kLoDelta >> 4);
+          ptx::mma_tf32(tmem, ad, bd + lo_step, idesc, 1u);
+          ptx::mma_tf32(tmem, ad + lo_step, bd, idesc, 1u);
+        }
       }
       ptx::mma_commit(&empty[stage]);
     }
@@ -357,20 +399,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool PRECISE>
 int launch(const Args& a, int splits, cudaStream_t stream) {
-  constexpr size_t kStageBytes = (kBM + BN) * kBK * 4;
+  constexpr size_t kStageBytes = (kBM + BN) * kBK * 4 * (PRECISE ? 2 : 1);
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(conv_igemm_kernel<MODE, BN>,
+    cudaFuncSetAttribute(conv_igemm_kernel<MODE, BN, PRECISE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
   dim3 grid((a.M + kBM - 1) / kBM, (a.Ng + BN - 1) / BN, splits);
-  conv_igemm_kernel<MODE, BN><<<grid, kThreads, smem, stream>>>(a);
+  conv_igemm_kernel<MODE, BN, PRECISE><<<grid, kThreads, smem, stream>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
+
+int g_conv_math = 0;  // 0 = TF32, 1 = 3xTF32
 
 Args make_args(const accudnn_conv_desc* d, int mode) {
   Args a{};
@@ -406,8 +450,12 @@ int dispatch(Args a, int splits, cudaStream_t stream) {
   a.kb_per_split = (a.kb_total + splits - 1) / splits;
   splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
   a.atomic = splits > 1 ? 1 : 0;
-  if (a.Ng <= 64) return launch<MODE, 64>(a, splits, stream);
-  return launch<MODE, 128>(a, splits, stream);
+  if (g_conv_math == 1) {
+    if (a.Ng <= 64) return launch<MODE, 64, true>(a, splits, stream);
+    return launch<MODE, 128, true>(a, splits, stream);
+  }
+  if (a.Ng <= 64) return launch<MODE, 64, false>(a, splits, stream);
+  return launch<MODE, 128, false>(a, splits, stream);
 }
 
 // split-K factor: fill ~2 CTAs per SM when the output tile grid is small
@@ -469,3 +517,10 @@ extern "C" int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, co
   }
   return dispatch<WGRAD>(a, splits, stream);
 }
+
+extern "C" int accudnn_set_conv_math(int mode) {
+  if (mode != 0 && mode != 1) return static_cast<int>(cudaErrorInvalidValue);
+  accudnn::g_conv_math = mode;
+  return 0;
+}
+extern "C" int accudnn_get_conv_math(void) { return accudnn::g_conv_math; }

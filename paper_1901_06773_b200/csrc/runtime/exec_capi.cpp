@@ -1,0 +1,205 @@
+// C ABI of the executor (include/accudnn.h).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+
+#include <json.hpp>
+
+#include "accudnn.h"
+#include "executor.h"
+#include "net.h"
+
+using nlohmann::json;
+
+struct accudnn_exec {
+  std::unique_ptr<accudnn::Executor> ex;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+char* dup_out(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.data(), s.size() + 1);
+  return p;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  g_err.clear();
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const json::exception& e) {
+    g_err = std::string("malformed document: ") + e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* accudnn_rt_last_error(void) { return g_err.c_str(); }
+void accudnn_rt_free(void* p) { std::free(p); }
+
+int accudnn_net_export(const char* arch, int image, int classes, int k_base, int lookahead,
+                       char** network_json, char** describe_json) {
+  return guarded([&] {
+    const accudnn::Net net = accudnn::build_net(arch, image, classes);
+    if (network_json) *network_json = dup_out(accudnn::export_network_json(net, k_base, lookahead));
+    if (describe_json) *describe_json = dup_out(accudnn::describe_net_json(net));
+    return 0;
+  });
+}
+
+int accudnn_exec_create(const char* arch, int image, int classes, const char* mode,
+                        const char* network_json, const char* hardware_json,
+                        const char* plan_json, int k, int device, int lookahead,
+                        accudnn_exec** out) {
+  return guarded([&] {
+    accudnn::ExecConfig cfg;
+    cfg.arch = arch;
+    cfg.image = image;
+    cfg.classes = classes;
+    cfg.device = device;
+    cfg.lookahead = lookahead;
+    const accudnn::Net net = accudnn::build_net(arch, image, classes);
+    const int n = net.num_ops();
+    const std::string m = mode ? mode : "resident";
+    std::vector<char> swapped(static_cast<size_t>(n), 0);
+    if (m == "naive") {
+      swapped.assign(static_cast<size_t>(n), 1);
+    } else if (m == "dynamic") {
+      if (!plan_json) throw std::invalid_argument("dynamic mode needs a plan");
+      const json plan = json::parse(plan_json);
+      if (k <= 0) k = plan.at("k_star").get<int>();
+      swapped.assign(static_cast<size_t>(n), 1);
+      for (const auto& name : plan.at("pinned_objects")) {
+        const std::string s = name.get<std::string>();
+        if (s.rfind("fm", 0) != 0) throw std::invalid_argument("plan pins a non-featuremap: " + s);
+        const int layer = std::atoi(s.c_str() + 2);
+        if (layer < 1 || layer > n) throw std::invalid_argument("plan pins unknown object " + s);
+        swapped[static_cast<size_t>(layer - 1)] = 0;
+      }
+    } else if (m != "resident") {
+      throw std::invalid_argument("unknown mode '" + m + "'");
+    }
+    if (k <= 0) throw std::invalid_argument("k must be positive");
+    cfg.k = k;
+    if (hardware_json) {
+      const json hw = json::parse(hardware_json);
+      cfg.budget = hw.at("memory_budget_bytes").get<unsigned long long>();
+      unsigned long long pg = 0;
+      if (network_json) {
+        const json nj = json::parse(network_json);
+        for (const auto& l : nj.at("layers"))
+          pg += l.at("param_bytes").get<unsigned long long>() +
+                l.at("grad_bytes").get<unsigned long long>();
+      }
+      cfg.fixed_allowance = hw.at("m_others_bytes").get<unsigned long long>() + pg;
+      if (!network_json) cfg.fixed_allowance = 0;
+    }
+    auto h = std::make_unique<accudnn_exec>();
+    h->ex = std::make_unique<accudnn::Executor>(cfg, swapped);
+    *out = h.release();
+    return 0;
+  });
+}
+
+int accudnn_exec_destroy(accudnn_exec* ex) {
+  return guarded([&] {
+    delete ex;
+    return 0;
+  });
+}
+
+long long accudnn_exec_num_params(accudnn_exec* ex) { return ex ? ex->ex->net().n_params : -1; }
+long long accudnn_exec_num_stats(accudnn_exec* ex) { return ex ? ex->ex->net().n_stats : -1; }
+
+int accudnn_exec_set_params(accudnn_exec* ex, const float* host, long long n) {
+  return guarded([&] {
+    ex->ex->set_params(host, n);
+    return 0;
+  });
+}
+int accudnn_exec_get_params(accudnn_exec* ex, float* host, long long n) {
+  return guarded([&] {
+    ex->ex->get_params(host, n);
+    return 0;
+  });
+}
+int accudnn_exec_get_grads(accudnn_exec* ex, float* host, long long n) {
+  return guarded([&] {
+    ex->ex->get_grads(host, n);
+    return 0;
+  });
+}
+int accudnn_exec_get_stats(accudnn_exec* ex, float* host, long long n) {
+  return guarded([&] {
+    ex->ex->get_stats(host, n);
+    return 0;
+  });
+}
+int accudnn_exec_set_graph(accudnn_exec* ex, int enable) {
+  ex->ex->use_graph = enable != 0;
+  return 0;
+}
+
+int accudnn_exec_step(accudnn_exec* ex, const float* images, const int* labels, int host_inputs,
+                      float lr, int update, int profile, accudnn_step_stats* out) {
+  return guarded([&] {
+    const accudnn::StepStats s = ex->ex->step(images, labels, host_inputs, lr, update, profile);
+    if (out) {
+      out->loss = s.loss;
+      out->iter_ms = s.iter_ms;
+      out->exposed_swap_ms = s.exposed_swap_ms;
+      out->allreduce_ms = s.allreduce_ms;
+      out->peak_bytes = s.peak_bytes;
+      out->swapped_bytes = s.swapped_bytes;
+    }
+    return 0;
+  });
+}
+
+int accudnn_exec_memory(accudnn_exec* ex, unsigned long long* arena, unsigned long long* fixed) {
+  if (arena) *arena = ex->ex->arena_bytes();
+  if (fixed) *fixed = ex->ex->fixed_bytes();
+  return 0;
+}
+
+int accudnn_exec_launches(accudnn_exec* ex) { return ex->ex->graph_launches(); }
+
+int accudnn_exec_trace(accudnn_exec* ex, char** csv) {
+  return guarded([&] {
+    *csv = dup_out(ex->ex->trace_csv());
+    return 0;
+  });
+}
+
+int accudnn_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return 3;
+  std::memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int accudnn_exec_set_comm(accudnn_exec* ex, const void* uid128, int rank, int world) {
+  return guarded([&] {
+    ex->ex->set_comm(uid128, rank, world);
+    return 0;
+  });
+}
+
+}  // extern "C"

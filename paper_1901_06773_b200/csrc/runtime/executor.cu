@@ -1,0 +1,624 @@
+// Swap executor (see executor.h).
+#include "executor.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+
+#include "accudnn_kernels.h"
+
+namespace accudnn {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ckl(int rc, const char* what) { ck(static_cast<cudaError_t>(rc), what); }
+void ckn(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+constexpr long long kAlign = 512;
+
+}  // namespace
+
+struct Executor::Impl {
+  LifetimeModel lm;
+  std::vector<char> swapped;
+  int n = 0;
+  // device memory
+  char* arena = nullptr;
+  float* params = nullptr;
+  float* grads = nullptr;
+  float* momentum_buf = nullptr;
+  float* stats = nullptr;
+  void* bn_ws = nullptr;
+  float* image = nullptr;        // NHWC4
+  float* image_nchw = nullptr;   // staging for the host copy
+  int* labels = nullptr;
+  float* loss = nullptr;
+  float* loss_host = nullptr;    // pinned
+  std::vector<float*> host_store;  // pinned host copies of swapped featuremaps
+  // streams / events
+  cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr, comm_stream = nullptr;
+  std::vector<cudaEvent_t> step_done;   // per step
+  std::vector<cudaEvent_t> d2h_done;    // per tensor
+  std::vector<cudaEvent_t> h2d_done;    // per tensor
+  std::vector<cudaEvent_t> phase_begin, phase_end;  // profiling
+  cudaEvent_t iter_begin = nullptr, iter_end = nullptr, comm_done = nullptr;
+  std::vector<cudaEvent_t> bucket_ready;
+  // per-instance region predecessors: (instance index)
+  std::vector<std::vector<int>> preds;
+  // per-step actions
+  std::vector<std::vector<int>> prefetch_at;  // step -> tensors to prefetch
+  std::vector<std::vector<int>> offload_at;   // step -> tensors to offload
+  std::vector<std::vector<int>> first_compute_write;  // step -> instances written first
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  bool first_step = true;
+  // CUDA graph of the iteration (fixed lr/update are baked in)
+  cudaGraphExec_t graph = nullptr;
+  float graph_lr = -1.f;
+  int graph_update = -1;
+};
+
+Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
+    : impl_(std::make_unique<Impl>()), cfg_(cfg) {
+  net_ = build_net(cfg.arch, cfg.image, cfg.classes);
+  Impl& I = *impl_;
+  I.n = net_.num_ops();
+  const int n = I.n;
+  if (!swapped.empty() && static_cast<int>(swapped.size()) != n)
+    throw std::invalid_argument("swap mask does not match the network");
+  I.swapped = swapped.empty() ? std::vector<char>(static_cast<size_t>(n), 0) : swapped;
+  ck(cudaSetDevice(cfg.device), "cudaSetDevice");
+
+  // ---- static arena plan ----
+  I.lm = build_lifetimes(net_, cfg.k, I.swapped, cfg.lookahead, kAlign);
+  std::vector<int> order(I.lm.inst.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const Instance& x = I.lm.inst[static_cast<size_t>(a)];
+    const Instance& y = I.lm.inst[static_cast<size_t>(b)];
+    if (x.bytes != y.bytes) return x.bytes > y.bytes;
+    return x.first < y.first;
+  });
+  std::vector<int> placed;
+  long long arena = 0;
+  for (int id : order) {
+    Instance& x = I.lm.inst[static_cast<size_t>(id)];
+    // occupied ranges of time-overlapping placed instances, sorted by offset
+    std::vector<std::pair<long long, long long>> busy;
+    for (int p : placed) {
+      const Instance& y = I.lm.inst[static_cast<size_t>(p)];
+      if (y.first <= x.last && x.first <= y.last) busy.emplace_back(y.offset, y.offset + y.bytes);
+    }
+    std::sort(busy.begin(), busy.end());
+    long long off = 0;
+    for (const auto& [lo, hi] : busy) {
+      if (off + x.bytes <= lo) break;
+      off = std::max(off, hi);
+    }
+    x.offset = off;
+    arena = std::max(arena, off + x.bytes);
+    placed.push_back(id);
+  }
+  arena_bytes_ = static_cast<unsigned long long>(arena);
+
+  // region predecessors: earlier (in time) instances sharing bytes
+  I.preds.assign(I.lm.inst.size(), {});
+  for (size_t a = 0; a < I.lm.inst.size(); ++a) {
+    const Instance& x = I.lm.inst[a];
+    for (size_t b = 0; b < I.lm.inst.size(); ++b) {
+      const Instance& y = I.lm.inst[b];
+      if (a == b || y.last >= x.first) continue;
+      if (y.offset < x.offset + x.bytes && x.offset < y.offset + y.bytes)
+        I.preds[a].push_back(static_cast<int>(b));
+    }
+  }
+  I.prefetch_at.assign(static_cast<size_t>(2 * n + 2), {});
+  I.offload_at.assign(static_cast<size_t>(2 * n + 2), {});
+  I.first_compute_write.assign(static_cast<size_t>(2 * n + 2), {});
+  for (int t = 0; t < n; ++t) {
+    if (!I.swapped[static_cast<size_t>(t)]) continue;
+    I.offload_at[static_cast<size_t>(fwd_step(t))].push_back(t);
+    const Instance& p = I.lm.inst[static_cast<size_t>(I.lm.pre_inst[static_cast<size_t>(t)])];
+    I.prefetch_at[static_cast<size_t>(p.first)].push_back(t);
+  }
+  for (size_t i = 0; i < I.lm.inst.size(); ++i)
+    if (I.lm.inst[i].kind != InstKind::act_prefetched)
+      I.first_compute_write[static_cast<size_t>(I.lm.inst[i].first)].push_back(static_cast<int>(i));
+
+  // ---- fixed allocations (the planner's fixed overhead) ----
+  const long long k = cfg.k;
+  const size_t pbytes = sizeof(float) * static_cast<size_t>(net_.n_params);
+  const size_t sbytes = sizeof(float) * static_cast<size_t>(std::max<long long>(4, net_.n_stats));
+  const size_t wsbytes = accudnn_bn_workspace_bytes(std::max(4, net_.max_bn_channels));
+  const size_t img4 = sizeof(float) * static_cast<size_t>(k) * cfg.image * cfg.image * net_.in_c4;
+  const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg.image * cfg.image * net_.in_c;
+  fixed_bytes_ = 3 * pbytes + sbytes + wsbytes + img4 + img3 + sizeof(int) * k + 256;
+  if (cfg.budget) {
+    if (cfg.fixed_allowance && fixed_bytes_ > cfg.fixed_allowance)
+      throw std::runtime_error("fixed device allocations (" + std::to_string(fixed_bytes_) +
+                               " B) exceed the planner's fixed overhead (" +
+                               std::to_string(cfg.fixed_allowance) + " B)");
+    if (fixed_bytes_ + arena_bytes_ > cfg.budget)
+      throw std::runtime_error("executor arena " + std::to_string(arena_bytes_) +
+                               " B + fixed " + std::to_string(fixed_bytes_) +
+                               " B exceed the device budget " + std::to_string(cfg.budget));
+  }
+  ck(cudaMalloc(&I.arena, static_cast<size_t>(std::max<long long>(arena, kAlign))), "arena");
+  ck(cudaMalloc(&I.params, pbytes), "params");
+  ck(cudaMalloc(&I.grads, pbytes), "grads");
+  ck(cudaMalloc(&I.momentum_buf, pbytes), "momentum");
+  ck(cudaMalloc(&I.stats, sbytes), "stats");
+  ck(cudaMalloc(&I.bn_ws, wsbytes), "bn ws");
+  ck(cudaMalloc(&I.image, img4), "image");
+  ck(cudaMalloc(&I.image_nchw, img3), "image staging");
+  ck(cudaMalloc(&I.labels, sizeof(int) * k), "labels");
+  ck(cudaMalloc(&I.loss, 256), "loss");
+  ck(cudaMallocHost(&I.loss_host, sizeof(float)), "loss host");
+  ck(cudaMemset(I.params, 0, pbytes), "memset");
+  ck(cudaMemset(I.grads, 0, pbytes), "memset");
+  ck(cudaMemset(I.momentum_buf, 0, pbytes), "memset");
+  ck(cudaMemset(I.stats, 0, sbytes), "memset");
+  // running variance starts at 1
+  {
+    std::vector<float> st(static_cast<size_t>(std::max<long long>(4, net_.n_stats)), 0.f);
+    for (const Op& op : net_.ops)
+      if (op.stat_off >= 0)
+        for (int c = 0; c < op.channels; ++c)
+          st[static_cast<size_t>(op.stat_off + 3 * op.channels + c)] = 1.f;
+    ck(cudaMemcpy(I.stats, st.data(), sbytes, cudaMemcpyHostToDevice), "stats init");
+  }
+  I.host_store.assign(static_cast<size_t>(n), nullptr);
+  for (int t = 0; t < n; ++t)
+    if (I.swapped[static_cast<size_t>(t)]) {
+      const Instance& a = I.lm.inst[static_cast<size_t>(I.lm.act_inst[static_cast<size_t>(t)])];
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&I.host_store[static_cast<size_t>(t)]),
+                       static_cast<size_t>(a.bytes), cudaHostAllocDefault),
+         "pinned host store");
+    }
+
+  ck(cudaStreamCreateWithFlags(&I.compute, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&I.d2h, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&I.h2d, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&I.comm_stream, cudaStreamNonBlocking), "stream");
+  auto mk = [](std::vector<cudaEvent_t>& v, size_t cnt, bool timing) {
+    v.assign(cnt, nullptr);
+    for (auto& e : v)
+      ck(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming),
+         "event");
+  };
+  mk(I.step_done, static_cast<size_t>(2 * n + 2), false);
+  mk(I.d2h_done, static_cast<size_t>(n), false);
+  mk(I.h2d_done, static_cast<size_t>(n), false);
+  mk(I.phase_begin, static_cast<size_t>(2 * n + 2), true);
+  mk(I.phase_end, static_cast<size_t>(2 * n + 2), true);
+  ck(cudaEventCreate(&I.iter_begin), "event");
+  ck(cudaEventCreate(&I.iter_end), "event");
+  ck(cudaEventCreateWithFlags(&I.comm_done, cudaEventDisableTiming), "event");
+}
+
+Executor::~Executor() {
+  Impl& I = *impl_;
+  if (I.graph) cudaGraphExecDestroy(I.graph);
+  if (I.comm) ncclCommDestroy(I.comm);
+  for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
+                  &I.bucket_ready})
+    for (cudaEvent_t e : *v)
+      if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done})
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {I.compute, I.d2h, I.h2d, I.comm_stream})
+    if (s) cudaStreamDestroy(s);
+  for (float* h : I.host_store)
+    if (h) cudaFreeHost(h);
+  if (I.loss_host) cudaFreeHost(I.loss_host);
+  for (void* p : {static_cast<void*>(I.arena), static_cast<void*>(I.params),
+                  static_cast<void*>(I.grads), static_cast<void*>(I.momentum_buf),
+                  static_cast<void*>(I.stats), I.bn_ws, static_cast<void*>(I.image),
+                  static_cast<void*>(I.image_nchw), static_cast<void*>(I.labels),
+                  static_cast<void*>(I.loss)})
+    if (p) cudaFree(p);
+}
+
+void Executor::set_params(const float* host, long long n) {
+  if (n != net_.n_params) throw std::invalid_argument("parameter count mismatch");
+  ck(cudaMemcpy(impl_->params, host, sizeof(float) * n, cudaMemcpyHostToDevice), "set_params");
+  impl_->first_step = true;
+}
+void Executor::get_params(float* host, long long n) {
+  if (n != net_.n_params) throw std::invalid_argument("parameter count mismatch");
+  ck(cudaMemcpy(host, impl_->params, sizeof(float) * n, cudaMemcpyDeviceToHost), "get_params");
+}
+void Executor::get_grads(float* host, long long n) {
+  if (n != net_.n_params) throw std::invalid_argument("parameter count mismatch");
+  ck(cudaMemcpy(host, impl_->grads, sizeof(float) * n, cudaMemcpyDeviceToHost), "get_grads");
+}
+void Executor::get_stats(float* host, long long n) {
+  if (n != net_.n_stats) throw std::invalid_argument("stats count mismatch");
+  ck(cudaMemcpy(host, impl_->stats, sizeof(float) * n, cudaMemcpyDeviceToHost), "get_stats");
+}
+
+void Executor::set_comm(const void* uid, int rank, int world) {
+  Impl& I = *impl_;
+  if (world <= 1) return;
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ckn(ncclCommInitRank(&I.comm, world, id, rank), "ncclCommInitRank");
+  I.rank = rank;
+  I.world = world;
+}
+
+StepStats Executor::step(const void* images, const int* labels, int host_inputs, float lr,
+                         int update, int profile) {
+  Impl& I = *impl_;
+  const int n = I.n;
+  const int k = cfg_.k;
+  const Net& net = net_;
+  cudaStream_t cs = I.compute;
+  void* csv = static_cast<void*>(cs);
+  StepStats st;
+
+  auto act = [&](int t, int step) -> float* {
+    if (t == kImage) return I.image;
+    const size_t u = static_cast<size_t>(t);
+    int id = I.lm.act_inst[u];
+    if (I.lm.pre_inst[u] >= 0 && step >= I.lm.inst[static_cast<size_t>(I.lm.pre_inst[u])].first)
+      id = I.lm.pre_inst[u];
+    return reinterpret_cast<float*>(I.arena + I.lm.inst[static_cast<size_t>(id)].offset);
+  };
+  auto grad = [&](int t) -> float* {
+    const int id = I.lm.grad_inst[static_cast<size_t>(t)];
+    if (id < 0) throw std::logic_error("tensor without gradient buffer");
+    return reinterpret_cast<float*>(I.arena + I.lm.inst[static_cast<size_t>(id)].offset);
+  };
+  auto beta_for = [&](int x, int op) { return I.lm.grad_first_writer[static_cast<size_t>(x)] == op ? 0 : 1; };
+  auto elems = [&](int t) {
+    return static_cast<long long>(k) * net.shape[static_cast<size_t>(t)].per_image();
+  };
+  auto conv_desc = [&](const Op& op) {
+    accudnn_conv_desc d{};
+    if (op.kind == OpKind::fc) {
+      d = accudnn_conv_desc{k, 1, 1, op.cin, op.cout, 1, 1, 1, 0, 1, 1};
+      return d;
+    }
+    const int in_h = op.in0 == kImage ? net.image : net.shape[static_cast<size_t>(op.in0)].h;
+    const int in_w = op.in0 == kImage ? net.image : net.shape[static_cast<size_t>(op.in0)].w;
+    const TensorShape& so = net.shape[static_cast<size_t>(&op - net.ops.data())];
+    d = accudnn_conv_desc{k, in_h, in_w, op.cin, op.cout, op.r, op.s, op.stride, op.pad, so.h, so.w};
+    return d;
+  };
+
+  // ---- one forward op ----
+  auto forward = [&](int o, int s) {
+    const Op& op = net.ops[static_cast<size_t>(o)];
+    const TensorShape& so = net.shape[static_cast<size_t>(o)];
+    float* y = act(o, s);
+    switch (op.kind) {
+      case OpKind::conv: {
+        const accudnn_conv_desc d = conv_desc(op);
+        ckl(accudnn_conv_fwd(&d, act(op.in0, s), I.params + op.w_off, y, 0, csv), "conv fwd");
+        break;
+      }
+      case OpKind::fc: {
+        const accudnn_conv_desc d = conv_desc(op);
+        ckl(accudnn_conv_fwd(&d, act(op.in0, s), I.params + op.w_off, y, 0, csv), "fc fwd");
+        ckl(accudnn_bias_add(y, I.params + op.b_off, k, op.cout, csv), "bias");
+        break;
+      }
+      case OpKind::bn:
+      case OpKind::bn_relu: {
+        const int C = op.channels;
+        float* sp = I.stats + op.stat_off;
+        ckl(accudnn_bn_fwd(act(op.in0, s), elems(o) / C, C, I.params + op.g_off,
+                           I.params + op.beta_off, cfg_.bn_eps, op.kind == OpKind::bn_relu, y,
+                           sp, sp + C, sp + 2 * C, sp + 3 * C, cfg_.bn_momentum, I.bn_ws, csv),
+            "bn fwd");
+        break;
+      }
+      case OpKind::relu:
+        ckl(accudnn_relu_fwd(act(op.in0, s), y, elems(o), csv), "relu fwd");
+        break;
+      case OpKind::add:
+        ckl(accudnn_add_fwd(act(op.in0, s), act(op.in1, s), y, elems(o), csv), "add fwd");
+        break;
+      case OpKind::maxpool: {
+        const TensorShape& si = net.shape[static_cast<size_t>(op.in0)];
+        ckl(accudnn_maxpool_fwd(act(op.in0, s), k, si.h, si.w, si.c, op.pk, op.pk, op.pstride,
+                                op.ppad, so.h, so.w, y, csv),
+            "maxpool fwd");
+        break;
+      }
+      case OpKind::avgpool: {
+        const TensorShape& si = net.shape[static_cast<size_t>(op.in0)];
+        ckl(accudnn_avgpool_fwd(act(op.in0, s), k, si.h * si.w, si.c, y, csv), "avgpool fwd");
+        break;
+      }
+      case OpKind::xent:
+        ckl(accudnn_xent_fwd(act(op.in0, s), I.labels, k, net.classes, I.loss, csv), "xent fwd");
+        break;
+    }
+  };
+
+  // ---- one backward op ----
+  auto backward = [&](int o, int s) {
+    const Op& op = net.ops[static_cast<size_t>(o)];
+    switch (op.kind) {
+      case OpKind::conv:
+      case OpKind::fc: {
+        const accudnn_conv_desc d = conv_desc(op);
+        float* dy = grad(o);
+        ckl(accudnn_conv_wgrad(&d, act(op.in0, s), dy, I.grads + op.w_off, 0, 0, csv), "wgrad");
+        if (op.in0 != kImage)
+          ckl(accudnn_conv_dgrad(&d, dy, I.params + op.w_off, grad(op.in0), beta_for(op.in0, o),
+                                 csv),
+              "dgrad");
+        break;
+      }
+      case OpKind::bn:
+      case OpKind::bn_relu: {
+        const int C = op.channels;
+        float* sp = I.stats + op.stat_off;
+        ckl(accudnn_bn_bwd(act(op.in0, s), grad(o), elems(o) / C, C, I.params + op.g_off,
+                           I.params + op.beta_off, sp, sp + C, op.kind == OpKind::bn_relu,
+                           grad(op.in0), beta_for(op.in0, o), I.grads + op.g_off,
+                           I.grads + op.beta_off, I.bn_ws, csv),
+            "bn bwd");
+        break;
+      }
+      case OpKind::relu:
+        ckl(accudnn_relu_bwd(act(op.in0, s), grad(o), grad(op.in0), elems(o), beta_for(op.in0, o),
+                             csv),
+            "relu bwd");
+        break;
+      case OpKind::add:
+        for (int x : {op.in0, op.in1}) {
+          if (x < 0) continue;
+          if (I.lm.grad_group[static_cast<size_t>(x)] == I.lm.grad_group[static_cast<size_t>(o)])
+            continue;  // aliased pass-through
+          ckl(accudnn_copy(grad(o), grad(x), elems(o), beta_for(x, o), csv), "add bwd");
+        }
+        break;
+      case OpKind::maxpool: {
+        const TensorShape& si = net.shape[static_cast<size_t>(op.in0)];
+        const TensorShape& so = net.shape[static_cast<size_t>(o)];
+        if (beta_for(op.in0, o)) throw std::logic_error("maxpool input with several consumers");
+        ckl(accudnn_maxpool_bwd(act(op.in0, s), grad(o), k, si.h, si.w, si.c, op.pk, op.pk,
+                                op.pstride, op.ppad, so.h, so.w, grad(op.in0), csv),
+            "maxpool bwd");
+        break;
+      }
+      case OpKind::avgpool: {
+        const TensorShape& si = net.shape[static_cast<size_t>(op.in0)];
+        if (beta_for(op.in0, o)) throw std::logic_error("avgpool input with several consumers");
+        ckl(accudnn_avgpool_bwd(grad(o), k, si.h * si.w, si.c, grad(op.in0), csv), "avgpool bwd");
+        break;
+      }
+      case OpKind::xent: {
+        const Op& fc = net.ops[static_cast<size_t>(op.in0)];
+        if (fc.kind != OpKind::fc) throw std::logic_error("loss must follow the classifier");
+        ckl(accudnn_xent_bwd(act(op.in0, s), I.labels, k, net.classes, grad(op.in0),
+                             I.grads + fc.b_off, csv),
+            "xent bwd");
+        break;
+      }
+    }
+  };
+
+  // wait for everything a newly written instance's region depends on
+  auto wait_region = [&](int inst, cudaStream_t stream, bool same_as_compute) {
+    for (int p : I.preds[static_cast<size_t>(inst)]) {
+      const Instance& y = I.lm.inst[static_cast<size_t>(p)];
+      if (y.kind == InstKind::act && y.swapped)
+        ck(cudaStreamWaitEvent(stream, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
+      if (!same_as_compute) {
+        ck(cudaStreamWaitEvent(stream, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
+      }
+    }
+  };
+
+  // gradient all-reduce buckets over the completed prefix of the grads
+  std::vector<long long> prefix_after_step(static_cast<size_t>(2 * n + 2), 0);
+  {
+    long long done = 0;
+    for (int s = n + 1; s <= 2 * n; ++s) {
+      const int o = 2 * n + 1 - s;
+      auto extend = [&](int op_id) {
+        const Op& op = net.ops[static_cast<size_t>(op_id)];
+        long long end = -1;
+        if (op.w_off >= 0) end = std::max(end, op.w_off + static_cast<long long>(op.cout) * op.r * op.s * op.cin);
+        if (op.b_off >= 0) end = std::max(end, op.b_off + op.cout);
+        if (op.beta_off >= 0) end = std::max(end, op.beta_off + op.channels);
+        if (end > done) done = end;
+      };
+      if (o >= 1 && o < n) extend(o);
+      if (s == 2 * n) extend(0);
+      prefix_after_step[static_cast<size_t>(s)] = std::min(done, net.n_params);
+    }
+  }
+
+  auto enqueue_iteration = [&](bool capture) {
+    int launches = 0;
+    if (host_inputs && !capture) {
+      const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
+      ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyHostToDevice, cs), "h2d images");
+      ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyHostToDevice, cs), "h2d labels");
+    }
+    const float* src = (host_inputs || capture) ? I.image_nchw : static_cast<const float*>(images);
+    if (!host_inputs && !capture && labels)
+      ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyDeviceToDevice, cs), "labels");
+    ckl(accudnn_nchw_to_nhwc_pad(src, k, net.in_c, cfg_.image, cfg_.image, net.in_c4, I.image, csv),
+        "image layout");
+    ++launches;
+    long long reduced = 0;
+    const long long bucket = std::max<long long>(1, cfg_.bucket_bytes / 4);
+    bool comm_used = false;
+    for (int s = 1; s <= 2 * n; ++s) {
+      // swap-in: prefetches that may start at this step
+      for (int t : I.prefetch_at[static_cast<size_t>(s)]) {
+        const int pid = I.lm.pre_inst[static_cast<size_t>(t)];
+        const Instance& p = I.lm.inst[static_cast<size_t>(pid)];
+        ck(cudaStreamWaitEvent(I.h2d, I.d2h_done[static_cast<size_t>(t)], 0), "wait");
+        // region free: every earlier occupant finished (compute) and drained
+        for (int q : I.preds[static_cast<size_t>(pid)]) {
+          const Instance& y = I.lm.inst[static_cast<size_t>(q)];
+          if (y.kind == InstKind::act && y.swapped)
+            ck(cudaStreamWaitEvent(I.h2d, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
+          ck(cudaStreamWaitEvent(I.h2d, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
+        }
+        ck(cudaMemcpyAsync(I.arena + p.offset, I.host_store[static_cast<size_t>(t)],
+                           static_cast<size_t>(p.bytes), cudaMemcpyHostToDevice, I.h2d),
+           "prefetch");
+        ck(cudaEventRecord(I.h2d_done[static_cast<size_t>(t)], I.h2d), "record");
+      }
+      // compute: inputs that were prefetched must have landed
+      const bool fwd = s <= n;
+      std::vector<int> ops;
+      if (fwd) {
+        ops.push_back(s - 1);
+      } else {
+        const int o = 2 * n + 1 - s;
+        if (o >= 1 && o < n) ops.push_back(o);
+        if (s == 2 * n) ops.push_back(0);
+      }
+      for (int o : ops) {
+        const Op& op = net.ops[static_cast<size_t>(o)];
+        for (int x : {op.in0, op.in1})
+          if (x >= 0 && I.swapped[static_cast<size_t>(x)] && !fwd)
+            ck(cudaStreamWaitEvent(cs, I.h2d_done[static_cast<size_t>(x)], 0), "wait");
+      }
+      for (int inst : I.first_compute_write[static_cast<size_t>(s)]) wait_region(inst, cs, true);
+      if (profile && !capture) ck(cudaEventRecord(I.phase_begin[static_cast<size_t>(s)], cs), "rec");
+      for (int o : ops) {
+        if (fwd)
+          forward(o, s);
+        else
+          backward(o, s);
+        ++launches;
+      }
+      if (profile && !capture) ck(cudaEventRecord(I.phase_end[static_cast<size_t>(s)], cs), "rec");
+      ck(cudaEventRecord(I.step_done[static_cast<size_t>(s)], cs), "record");
+      // swap-out: offload what this step produced
+      for (int t : I.offload_at[static_cast<size_t>(s)]) {
+        const Instance& a = I.lm.inst[static_cast<size_t>(I.lm.act_inst[static_cast<size_t>(t)])];
+        ck(cudaStreamWaitEvent(I.d2h, I.step_done[static_cast<size_t>(s)], 0), "wait");
+        ck(cudaMemcpyAsync(I.host_store[static_cast<size_t>(t)], I.arena + a.offset,
+                           static_cast<size_t>(a.bytes), cudaMemcpyDeviceToHost, I.d2h),
+           "offload");
+        ck(cudaEventRecord(I.d2h_done[static_cast<size_t>(t)], I.d2h), "record");
+      }
+      // data parallel: all-reduce completed gradient buckets while the
+      // backward continues
+      if (I.comm && !fwd) {
+        const long long ready = prefix_after_step[static_cast<size_t>(s)];
+        if (ready - reduced >= bucket || (s == 2 * n && ready > reduced)) {
+          ck(cudaStreamWaitEvent(I.comm_stream, I.step_done[static_cast<size_t>(s)], 0), "wait");
+          ckn(ncclAllReduce(I.grads + reduced, I.grads + reduced,
+                            static_cast<size_t>(ready - reduced), ncclFloat, ncclSum, I.comm,
+                            I.comm_stream),
+              "ncclAllReduce");
+          reduced = ready;
+          comm_used = true;
+        }
+      }
+    }
+    if (comm_used) {
+      ck(cudaEventRecord(I.comm_done, I.comm_stream), "record");
+      ck(cudaStreamWaitEvent(cs, I.comm_done, 0), "wait");
+    }
+    // the copy streams rejoin the compute stream (graph capture needs it)
+    bool any_swap = false;
+    for (char c : I.swapped) any_swap = any_swap || c;
+    if (any_swap) {
+      ck(cudaEventRecord(I.step_done[0], I.d2h), "record");
+      ck(cudaStreamWaitEvent(cs, I.step_done[0], 0), "wait");
+      ck(cudaEventRecord(I.step_done[2 * n + 1], I.h2d), "record");
+      ck(cudaStreamWaitEvent(cs, I.step_done[2 * n + 1], 0), "wait");
+    }
+    if (update) {
+      ckl(accudnn_sgd_update(I.params, I.grads, I.momentum_buf, net.n_params, lr,
+                             cfg_.momentum, cfg_.weight_decay, 1.0f / static_cast<float>(I.world),
+                             I.first_step ? 1 : 0, csv),
+          "sgd");
+      ++launches;
+    }
+    return launches;
+  };
+
+  ck(cudaEventRecord(I.iter_begin, cs), "record");
+  const bool graph_ok = use_graph && !profile && update && !I.first_step;
+  if (graph_ok) {
+    if (host_inputs) {
+      const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
+      ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyHostToDevice, cs), "h2d images");
+      ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyHostToDevice, cs), "h2d labels");
+    } else {
+      const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
+      ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyDeviceToDevice, cs), "images");
+      ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyDeviceToDevice, cs), "labels");
+    }
+    if (!I.graph || I.graph_lr != lr || I.graph_update != update) {
+      if (I.graph) cudaGraphExecDestroy(I.graph);
+      I.graph = nullptr;
+      cudaGraph_t g;
+      ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture");
+      kernel_launches_ = enqueue_iteration(true);
+      ck(cudaStreamEndCapture(cs, &g), "end capture");
+      ck(cudaGraphInstantiate(&I.graph, g, 0), "instantiate");
+      cudaGraphDestroy(g);
+      I.graph_lr = lr;
+      I.graph_update = update;
+    }
+    ck(cudaGraphLaunch(I.graph, cs), "graph launch");
+  } else {
+    kernel_launches_ = enqueue_iteration(false);
+  }
+  ck(cudaEventRecord(I.iter_end, cs), "record");
+  ck(cudaMemcpyAsync(I.loss_host, I.loss, sizeof(float), cudaMemcpyDeviceToHost, cs), "loss d2h");
+  ck(cudaStreamSynchronize(cs), "step");
+  if (update) I.first_step = false;
+
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, I.iter_begin, I.iter_end), "elapsed");
+  st.loss = *I.loss_host;
+  st.iter_ms = ms;
+  st.peak_bytes = fixed_bytes_ + arena_bytes_;
+  for (int t = 0; t < n; ++t)
+    if (I.swapped[static_cast<size_t>(t)])
+      st.swapped_bytes += static_cast<unsigned long long>(
+          I.lm.inst[static_cast<size_t>(I.lm.act_inst[static_cast<size_t>(t)])].bytes);
+  if (profile) {
+    // exposed swap time: compute-stream gaps between consecutive phases
+    double busy = 0;
+    std::string tr = "phase,begin_ms,end_ms\n";
+    for (int s = 1; s <= 2 * n; ++s) {
+      float b = 0, e = 0;
+      ck(cudaEventElapsedTime(&b, I.iter_begin, I.phase_begin[static_cast<size_t>(s)]), "t");
+      ck(cudaEventElapsedTime(&e, I.iter_begin, I.phase_end[static_cast<size_t>(s)]), "t");
+      busy += e - b;
+      char line[96];
+      std::snprintf(line, sizeof line, "%d,%.6f,%.6f\n", s, b, e);
+      tr += line;
+    }
+    float first_b = 0, last_e = 0;
+    ck(cudaEventElapsedTime(&first_b, I.iter_begin, I.phase_begin[1]), "t");
+    ck(cudaEventElapsedTime(&last_e, I.iter_begin, I.phase_end[static_cast<size_t>(2 * n)]), "t");
+    st.exposed_swap_ms = std::max(0.0, (last_e - first_b) - busy);
+    trace_ = tr;
+  }
+  return st;
+}
+
+}  // namespace accudnn

@@ -1,0 +1,89 @@
+// Swap executor: realises one planned training iteration on a B200.
+//
+// Behavioural contract: /root/reference/proj/src/simulator.cpp:79-370 --
+// a compute stream running the 2N phases in order, a swap-out (D2H) stream
+// and a swap-in (H2D) stream working through the GMAP's offload/prefetch
+// queues in order, one FIFO copy engine per direction, a hard device-memory
+// cap.  Real CUDA streams and events replace the simulated ones:
+//   * every tensor instance (activation, prefetched activation, gradient
+//     group) gets a static offset in one capped arena (planned once per
+//     (net, k, pin set)); instance lifetimes come from net.h's lifetime
+//     model, the same one the exporter charged to the workspaces;
+//   * a region is reused only after its previous occupant's last reader
+//     (compute event) and drain (D2H event) completed;
+//   * an offload starts when its producing phase's kernels finish; a
+//     prefetch starts `lookahead` phases before its first backward reader
+//     once its offload landed in pinned host memory and its region is free;
+//   * the whole iteration (kernels, copies, event edges, the bucketed NCCL
+//     all-reduce and the SGD update) can be captured into one CUDA graph.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "net.h"
+
+namespace accudnn {
+
+struct ExecConfig {
+  std::string arch = "resnet152";
+  int image = 224;
+  int classes = 1000;
+  int k = 1;                       // per-GPU minibatch (k* of the plan)
+  unsigned long long budget = 0;   // device cap (hardware.json memory_budget_bytes)
+  unsigned long long fixed_allowance = 0;  // m_others + params + grads (planner's fixed)
+  int lookahead = 1;
+  float momentum = 0.9f;
+  float weight_decay = 1e-4f;
+  float bn_eps = 1e-5f;
+  float bn_momentum = 0.1f;
+  int device = 0;
+  long long bucket_bytes = 25LL << 20;
+};
+
+struct StepStats {
+  float loss = 0.f;
+  double iter_ms = 0;          // device time of the whole iteration
+  double exposed_swap_ms = 0;  // compute-stream stall on prefetches (profiled steps)
+  double allreduce_ms = 0;
+  unsigned long long peak_bytes = 0;  // fixed + arena (static plan)
+  unsigned long long swapped_bytes = 0;
+};
+
+class Executor {
+ public:
+  Executor(const ExecConfig& cfg, const std::vector<char>& swapped);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  const Net& net() const { return net_; }
+  void set_params(const float* host, long long n);
+  void get_params(float* host, long long n);
+  void get_grads(float* host, long long n);
+  void get_stats(float* host, long long n);
+  // images: NCHW fp32 [k][3][H][W]; labels int32 [k].  host_inputs = 1 copies
+  // from (pinned or pageable) host memory inside the step.
+  StepStats step(const void* images, const int* labels, int host_inputs, float lr, int update,
+                 int profile);
+  void set_comm(const void* nccl_unique_id, int rank, int world);
+  bool use_graph = false;
+  std::string trace_csv() const { return trace_; }
+  unsigned long long arena_bytes() const { return arena_bytes_; }
+  unsigned long long fixed_bytes() const { return fixed_bytes_; }
+  int graph_launches() const { return kernel_launches_; }
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+  Net net_;
+  ExecConfig cfg_;
+  std::string trace_;
+  unsigned long long arena_bytes_ = 0, fixed_bytes_ = 0;
+  int kernel_launches_ = 0;
+};
+
+}  // namespace accudnn

@@ -1,0 +1,190 @@
+"""Host-side mirror of the training step: network export, executor, one
+SGD step per call.
+
+Everything runs in libaccudnn.so (include/accudnn.h); this module only
+marshals arguments.  There is no fallback path: a missing library or a
+failing CUDA call raises.
+"""
+
+import ctypes
+import json
+
+import numpy as np
+
+from . import _native
+from ._exec_symbols import StepStats
+
+
+class ExecutorError(RuntimeError):
+    pass
+
+
+def _lib():
+    return _native.cuda_lib()
+
+
+def _take(ptr):
+    if not ptr:
+        return None
+    s = ctypes.string_at(ptr).decode()
+    _lib().accudnn_rt_free(ptr)
+    return s
+
+
+def _check(rc, what):
+    if rc != 0:
+        msg = _lib().accudnn_rt_last_error()
+        raise ExecutorError(f"{what} failed (rc={rc}): {msg.decode() if msg else ''}")
+
+
+def export_network(arch, image, classes, k_base=8, lookahead=1):
+    """(network.json text, op description dict) of an architecture.
+
+    network.json follows the reference format (model_ir.cpp:87-144): one
+    LayerDecl per executed op, featuremap = the op's output, workspace =
+    every other byte the executor holds in that layer's phases."""
+    a, b = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(_lib().accudnn_net_export(arch.encode(), int(image), int(classes), int(k_base),
+                                     int(lookahead), ctypes.byref(a), ctypes.byref(b)),
+           "net export")
+    return _take(a.value), json.loads(_take(b.value))
+
+
+def hardware_json(budget_bytes, m_others_bytes, pcie_bytes_per_s, delta_sync_s=0.0):
+    return json.dumps({"format_version": 1, "memory_budget_bytes": int(budget_bytes),
+                       "m_others_bytes": int(m_others_bytes), "delta_sync_s": float(delta_sync_s),
+                       "pcie_nominal_bytes_per_s": float(pcie_bytes_per_s)}, indent=2) + "\n"
+
+
+def default_m_others(describe, image):
+    """Fixed device bytes outside params+grads: the momentum buffer, BN
+    statistics and a staging allowance for the input batch (the paper's
+    "pre-cached inputs and fixed overheads")."""
+    momentum = 4 * describe["n_params"]
+    stats = 4 * describe["n_stats"]
+    staging = (96 << 20) if image >= 128 else (32 << 20)
+    return momentum + stats + staging
+
+
+def init_params(describe, seed=0):
+    """torchvision-style initialisation of the flat parameter vector:
+    Kaiming-normal (fan_out, ReLU) convs, BN gamma=1 / beta=0, FC uniform
+    +-1/sqrt(fan_in)."""
+    rng = np.random.default_rng(seed)
+    p = np.zeros(describe["n_params"], dtype=np.float32)
+    for op in describe["ops"]:
+        if op["kind"] == "conv":
+            cout, cin, r = op["cout"], op["cin"], op["r"]
+            std = (2.0 / (cout * r * r)) ** 0.5
+            w = rng.standard_normal((cout, r, r, cin)).astype(np.float32) * std
+            if op["in0"] == -2:  # zero the padded input channel
+                w[..., describe["in_channels"]:] = 0.0
+            p[op["w_off"]:op["w_off"] + w.size] = w.ravel()
+        elif op["kind"] == "fc":
+            cout, cin = op["cout"], op["cin"]
+            bound = 1.0 / cin ** 0.5
+            p[op["w_off"]:op["w_off"] + cout * cin] = rng.uniform(-bound, bound, cout * cin)
+            p[op["b_off"]:op["b_off"] + cout] = rng.uniform(-bound, bound, cout)
+        elif op["kind"] in ("bn", "bn_relu"):
+            c = op["channels"]
+            p[op["g_off"]:op["g_off"] + c] = 1.0
+            p[op["beta_off"]:op["beta_off"] + c] = 0.0
+    return p
+
+
+class Executor:
+    """One training-step executor on one GPU (include/accudnn.h).
+
+    mode: "resident" | "naive" | "dynamic" (plan_json's pin set)."""
+
+    def __init__(self, arch, image, classes, k=0, mode="resident", plan_json=None,
+                 network_json=None, hardware_json=None, device=0, lookahead=1):
+        self.lib = _lib()
+        self.arch, self.image, self.classes = arch, image, classes
+        h = ctypes.c_void_p()
+        enc = lambda s: s.encode() if isinstance(s, str) else s  # noqa: E731
+        _check(self.lib.accudnn_exec_create(arch.encode(), int(image), int(classes), enc(mode),
+                                            enc(network_json), enc(hardware_json),
+                                            enc(plan_json), int(k), int(device), int(lookahead),
+                                            ctypes.byref(h)), "executor create")
+        self.h = h
+        if k <= 0:
+            k = json.loads(plan_json)["k_star"]
+        self.k = k
+        self.n_params = self.lib.accudnn_exec_num_params(h)
+        self.n_stats = self.lib.accudnn_exec_num_stats(h)
+
+    def close(self):
+        if self.h:
+            self.lib.accudnn_exec_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_params(self, flat):
+        flat = np.ascontiguousarray(flat, dtype=np.float32)
+        _check(self.lib.accudnn_exec_set_params(self.h, flat.ctypes.data, flat.size), "set_params")
+
+    def _get(self, fn, n):
+        out = np.empty(n, dtype=np.float32)
+        _check(fn(self.h, out.ctypes.data, n), "copy out")
+        return out
+
+    def get_params(self):
+        return self._get(self.lib.accudnn_exec_get_params, self.n_params)
+
+    def get_grads(self):
+        return self._get(self.lib.accudnn_exec_get_grads, self.n_params)
+
+    def get_stats(self):
+        return self._get(self.lib.accudnn_exec_get_stats, self.n_stats)
+
+    def set_graph(self, enable=True):
+        self.lib.accudnn_exec_set_graph(self.h, 1 if enable else 0)
+
+    def memory(self):
+        a, f = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        self.lib.accudnn_exec_memory(self.h, ctypes.byref(a), ctypes.byref(f))
+        return a.value, f.value
+
+    def launches(self):
+        return self.lib.accudnn_exec_launches(self.h)
+
+    def trace(self):
+        p = ctypes.c_void_p()
+        _check(self.lib.accudnn_exec_trace(self.h, ctypes.byref(p)), "trace")
+        return _take(p.value)
+
+    def step(self, images, labels, lr=0.1, update=True, profile=False):
+        """images: NCHW float32 [k,3,H,W]; labels int32 [k].  numpy arrays (or
+        CPU torch tensors) are copied from host memory inside the step; CUDA
+        torch tensors are used in place."""
+        host = 1
+        if hasattr(images, "is_cuda") and images.is_cuda:
+            host = 0
+            ip, lp = images.data_ptr(), labels.data_ptr()
+        elif hasattr(images, "data_ptr"):
+            ip, lp = images.data_ptr(), labels.data_ptr()
+        else:
+            images = np.ascontiguousarray(images, dtype=np.float32)
+            labels = np.ascontiguousarray(labels, dtype=np.int32)
+            ip, lp = images.ctypes.data, labels.ctypes.data
+        st = StepStats()
+        _check(self.lib.accudnn_exec_step(self.h, ip, lp, host, float(lr), 1 if update else 0,
+                                          1 if profile else 0, ctypes.byref(st)), "step")
+        return {"loss": st.loss, "iter_ms": st.iter_ms, "exposed_swap_ms": st.exposed_swap_ms,
+                "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes}
+
+    def set_comm(self, uid_bytes, rank, world):
+        buf = ctypes.create_string_buffer(bytes(uid_bytes), 128)
+        _check(self.lib.accudnn_exec_set_comm(self.h, buf, int(rank), int(world)), "set_comm")
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib().accudnn_nccl_unique_id(buf), "ncclGetUniqueId")
+    return buf.raw

@@ -1,0 +1,155 @@
+"""End-to-end parity of the B200 training step against the CPU fp32 oracle
+(oracle/resnet_torch.py) on the same architecture, weights and inputs.
+
+Tolerances (stated): convolutions run on TF32 tensor cores (10-bit
+mantissa, FP32 accumulation), everything else in FP32.  We require
+  loss:        |rel err| < 2e-3
+  gradients:   relative L2 error of the flat gradient vector < 2e-2
+  parameters after 3 SGD steps: relative L2 error < 1e-4
+and, between the swap modes of the executor (resident / naive / dynamic),
+identical results up to split-K atomic ordering (rel L2 < 1e-5).
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+from paper_1901_06773_b200 import trainer  # noqa: E402
+from resnet_torch import TorchResNet  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("resnet20", 32, 12, 4), ("resnet50", 64, 8, 8), ("resnet164", 32, 12, 8)]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def data(k, image, classes, seed=0):
+    g = np.random.default_rng(seed)
+    x = g.standard_normal((k, 3, image, image)).astype(np.float32)
+    y = g.integers(0, classes, size=k).astype(np.int32)
+    return x, y
+
+
+@pytest.fixture
+def precise():
+    """3xTF32 convolutions for the duration of a test."""
+    from paper_1901_06773_b200 import _native
+    lib = _native.cuda_lib()
+    lib.accudnn_set_conv_math(1)
+    yield
+    lib.accudnn_set_conv_math(0)
+
+
+def run_case(arch, image, classes, k, seed=1):
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=seed)
+    ex = trainer.Executor(arch, image, classes, k=k)
+    ex.set_params(params)
+    x, y = data(k, image, classes)
+    out = ex.step(x, y, lr=0.0, update=False)
+    return desc, params, x, y, out["loss"], ex.get_grads().astype(np.float64)
+
+
+def oracle(desc, params, x, y, dtype=torch.float32, conv_math="exact"):
+    loss, g, _, _ = TorchResNet(desc, dtype, conv_math).step(
+        params, torch.zeros(desc["n_stats"]), None, x, y, lr=0.0, update=False)
+    return loss, g
+
+
+@pytest.mark.parametrize("arch,image,classes,k", CASES)
+def test_step_fp32_mode_matches_fp32_oracle(cuda_dev, precise, arch, image, classes, k):
+    """3xTF32 convolutions: the device step is as close to the float64
+    ground truth as PyTorch's own fp32 CPU step (within 3x its error, or
+    1e-5 relative), for the loss and the full flat gradient vector."""
+    desc, params, x, y, loss, g = run_case(arch, image, classes, k)
+    l64, g64 = oracle(desc, params, x, y, torch.float64)
+    l32, g32 = oracle(desc, params, x, y, torch.float32)
+    e_dev_l, e_ref_l = abs(loss - l64) / abs(l64), abs(l32 - l64) / abs(l64)
+    e_dev_g, e_ref_g = rel(g, g64), rel(g32, g64)
+    assert e_dev_l <= max(3 * e_ref_l, 1e-5), (e_dev_l, e_ref_l)
+    assert e_dev_g <= max(3 * e_ref_g, 1e-5), (e_dev_g, e_ref_g)
+
+
+@pytest.mark.parametrize("arch,image,classes,k", CASES)
+def test_step_tf32_mode_matches_tf32_oracle(cuda_dev, arch, image, classes, k):
+    """TF32 tensor-core convolutions (training default): the deviation from
+    the float64 ground truth is the deviation of an fp32 CPU step whose
+    convolutions see TF32-truncated operands (within 3x, or 2e-3)."""
+    desc, params, x, y, loss, g = run_case(arch, image, classes, k)
+    l64, g64 = oracle(desc, params, x, y, torch.float64)
+    lt, gt = oracle(desc, params, x, y, torch.float32, "tf32")
+    e_dev_l, e_ref_l = abs(loss - l64) / abs(l64), abs(lt - l64) / abs(l64)
+    e_dev_g, e_ref_g = rel(g, g64), rel(gt, g64)
+    assert e_dev_l <= max(3 * e_ref_l, 2e-3), (e_dev_l, e_ref_l)
+    assert e_dev_g <= max(3 * e_ref_g, 2e-3), (e_dev_g, e_ref_g)
+
+
+def test_sgd_steps_match_oracle(cuda_dev, precise):
+    arch, image, classes, k = "resnet20", 32, 12, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    p0 = trainer.init_params(desc, seed=2)
+    ex = trainer.Executor(arch, image, classes, k=k)
+    ex.set_params(p0)
+    oracle = TorchResNet(desc)
+    stats = torch.zeros(desc["n_stats"])
+    p_ref, buf = p0.copy(), None
+    losses = []
+    for it in range(3):
+        x, y = data(k, image, classes, seed=10 + it)
+        out = ex.step(x, y, lr=0.05, update=True)
+        loss, _, p_ref, buf = oracle.step(p_ref, stats, buf, x, y, lr=0.05, first=(it == 0))
+        losses.append((out["loss"], loss))
+        assert abs(out["loss"] - loss) / abs(loss) < 5e-3, losses
+    assert rel(ex.get_params(), p_ref) < 1e-4, rel(ex.get_params(), p_ref)
+
+
+@pytest.mark.parametrize("mode", ["naive", "dynamic"])
+def test_swap_modes_agree_with_resident(cuda_dev, mode):
+    arch, image, classes, k = "resnet50", 64, 8, 2
+    net_json, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=3)
+    x, y = data(k, image, classes, seed=4)
+    ref = trainer.Executor(arch, image, classes, k=k)
+    ref.set_params(params)
+    r = ref.step(x, y, update=False)
+    g_ref = ref.get_grads()
+    plan = None
+    if mode == "dynamic":
+        n = len(desc["ops"])
+        # pin every third featuremap, swap the rest
+        plan = json.dumps({"k_star": k, "pinned_objects": [f"fm{l}" for l in range(1, n + 1, 3)]})
+    ex = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan)
+    ex.set_params(params)
+    out = ex.step(x, y, update=False, profile=True)
+    assert out["swapped_bytes"] > 0
+    assert abs(out["loss"] - r["loss"]) <= 1e-5 * abs(r["loss"])
+    assert rel(ex.get_grads(), g_ref) < 1e-5
+    arena_swap, _ = ex.memory()
+    arena_res, _ = ref.memory()
+    assert arena_swap < arena_res
+
+
+def test_cuda_graph_step_matches_eager(cuda_dev):
+    arch, image, classes, k = "resnet20", 32, 12, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=5)
+    a = trainer.Executor(arch, image, classes, k=k)
+    b = trainer.Executor(arch, image, classes, k=k)
+    a.set_params(params)
+    b.set_params(params)
+    b.set_graph(True)
+    for it in range(3):
+        x, y = data(k, image, classes, seed=20 + it)
+        la = a.step(x, y, lr=0.05)["loss"]
+        lb = b.step(x, y, lr=0.05)["loss"]
+        assert abs(la - lb) <= 1e-4 * abs(la)
+    assert rel(b.get_params(), a.get_params()) < 1e-5
