@@ -1,0 +1,416 @@
+"""ResNet-152 images/s at the tuner-chosen minibatch under a device memory
+cap on 1..8 B200s (BASELINE.json `metric`, configs[2]/[3]).
+
+A "step" is one full training iteration of the hot path at k* images per
+GPU: forward, backward, swap traffic of the plan, bucketed NCCL gradient
+all-reduce (N > 1), SGD-momentum update.  Before timing, the path's host
+side runs exactly as a user would: export network.json, fit model.json from
+the B200 profile CSVs (profiles/b200/, measured by tools/profile_b200.py),
+plan (Algorithm 2 + greedy pinning -> k*, pin set), adapted learning rate
+(Eq. 9), executor on the plan.
+
+  value  images/s with inputs already in HBM (device time, CUDA events on
+         the executor's compute stream, max over ranks)
+  e2e    images/s through the C ABI step with pinned HOST inputs: the H2D
+         copy of the batch and the loss read-back are inside the timed step
+
+`--impl reference` times the CPU implementation of the same step (oracle
+port: plain PyTorch fp32 on all host cores, oracle/resnet_torch.py) on a
+bounded sample, plus the reference planner (oracle/_ref) on the same
+documents.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--arch", default="resnet152")
+    ap.add_argument("--image", type=int, default=224)
+    ap.add_argument("--classes", type=int, default=1000)
+    ap.add_argument("--cap-gib", type=float, default=8.0)
+    ap.add_argument("--k", type=int, default=0, help="override k* (0 = tuner)")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2, help="images in the CPU baseline step")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def plan_for(args, network_json, hardware_json):
+    """fit model.json from the committed B200 profiles and run the tuner."""
+    from paper_1901_06773_b200 import planner, profiler
+    pdir = os.path.join(ROOT, "profiles", "b200")
+    cpath = os.path.join(pdir, f"{args.arch}_compute_profile.csv")
+    tpath = os.path.join(pdir, f"{args.arch}_transfer_profile.csv")
+    if os.path.exists(cpath) and os.path.exists(tpath):
+        comp, tran = open(cpath).read(), open(tpath).read()
+        source = os.path.relpath(cpath, ROOT)
+    else:  # profile live (first run on a new config)
+        ks = profiler.grid(32)
+        comp = profiler.profile_compute(args.arch, args.image, args.classes, network_json, ks)
+        tran = profiler.profile_transfer(network_json, ks)
+        source = "live"
+    model_json = planner.fit(network_json, [comp, tran], hardware_json, eta=0.95)
+    t0 = time.perf_counter()
+    if args.k > 0:
+        plan_json = planner.plan(network_json, hardware_json, model_json, k_override=args.k)
+    else:
+        plan_json = planner.plan(network_json, hardware_json, model_json)
+    plan_s = time.perf_counter() - t0
+    return model_json, plan_json, plan_s, source
+
+
+def conv_flops_per_image(desc):
+    f = 0.0
+    for op in desc["ops"]:
+        if op["kind"] in ("conv", "fc"):
+            h, w, c = op["out"]
+            fwd = 2.0 * h * w * op["cout"] * op["cin"] * op["r"] * op["r"]
+            f += fwd * (2.0 if op["in0"] == -2 else 3.0)
+    return f
+
+
+def kernel_launches_per_step(desc):
+    per = {"conv": (1, 2), "fc": (2, 2), "bn": (3, 3), "bn_relu": (3, 3), "relu": (1, 1),
+           "add": (1, 0), "maxpool": (1, 1), "avgpool": (1, 1), "xent": (1, 1)}
+    n = 2  # layout conversion + SGD
+    for op in desc["ops"]:
+        f, b = per[op["kind"]]
+        if op["kind"] == "conv" and op["in0"] == -2:
+            b = 1
+        n += f + b
+    return n
+
+
+def roofline_from_trace(desc, trace_csv, k, peak_tflops, n_ops):
+    """conv / fc phases of a profiled step -> achieved TFLOP/s of the implicit
+    GEMM kernels (phase j <= N: forward of op j-1; phase j > N: backward of op
+    2N+1-j, plus op 0 in phase 2N)."""
+    rows = [r.split(",") for r in trace_csv.strip().splitlines()[1:]]
+    t = {int(r[0]): float(r[2]) - float(r[1]) for r in rows}
+    ops = desc["ops"]
+    conv_ms, total_ms, conv_flops = 0.0, 0.0, 0.0
+    for j, ms in t.items():
+        total_ms += ms
+        ids = [j - 1] if j <= n_ops else ([2 * n_ops + 1 - j] if 2 * n_ops + 1 - j < n_ops else [])
+        if j == 2 * n_ops:
+            ids.append(0)
+        for o in ids:
+            op = ops[o]
+            if op["kind"] in ("conv", "fc"):
+                h, w, c = op["out"]
+                fwd = 2.0 * h * w * op["cout"] * op["cin"] * op["r"] * op["r"] * k
+                conv_flops += fwd if j <= n_ops else fwd * (1.0 if op["in0"] == -2 else 2.0)
+                conv_ms += ms / len(ids)
+    achieved = conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
+    return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_tflops,
+            "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4), "traffic": None,
+            "kernel": "conv_igemm_kernel (tcgen05 kind::tf32)",
+            "conv_share_of_step": round(conv_ms / total_ms, 4) if total_ms else None,
+            "flops_per_launch_note": "sum of conv/fc fwd+dgrad+wgrad FLOPs per step / sum of "
+                                     "their phase times (CUDA events on the compute stream)"}
+
+
+# ---------------------------------------------------------------------------
+def cpu_step_rate(arch, image, classes, k, threads, seed=0):
+    """oracle port: plain PyTorch fp32 training step on the host cores."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from resnet_torch import TorchResNet
+    from paper_1901_06773_b200 import trainer
+    torch.set_num_threads(threads)
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed)
+    g = np.random.default_rng(seed)
+    x = g.standard_normal((k, 3, image, image)).astype(np.float32)
+    y = g.integers(0, classes, size=k).astype(np.int32)
+    o = TorchResNet(desc)
+    stats = torch.zeros(desc["n_stats"])
+    o.step(params, stats, None, x, y, lr=0.1)  # warm-up
+    t0 = time.perf_counter()
+    o.step(params, stats, None, x, y, lr=0.1)
+    dt = time.perf_counter() - t0
+    return k / dt, dt
+
+
+def reference_planner_seconds(network_json, hardware_json, model_json):
+    path = os.path.join(ROOT, "oracle", "_ref", "libswapsched_ref.so")
+    if not os.path.exists(path):
+        return None
+    import ctypes
+    from paper_1901_06773_b200 import _native, planner
+    lib = ctypes.CDLL(path)
+    _native.declare_planner_symbols(lib, "oracle_")
+    t0 = time.perf_counter()
+    try:
+        planner.plan(network_json, hardware_json, model_json, lib=lib, prefix="oracle_", step=16)
+    except planner.PlannerError:
+        pass
+    return time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from paper_1901_06773_b200 import trainer
+    k = args.k or 24
+    rates = []
+    for _ in range(max(1, args.warmup)):
+        cpu_step_rate(args.arch, args.image, args.classes, args.cpu_sample, threads)
+    for _ in range(max(1, args.steps)):
+        r, _ = cpu_step_rate(args.arch, args.image, args.classes, args.cpu_sample, threads)
+        rates.append(r)
+    value = sum(rates) / len(rates)
+    line = {
+        "impl": "reference", "metric": "images/s (ResNet-152 training step, tuned minibatch, "
+        "device cap)", "value": round(value, 3), "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * args.cpu_sample / value, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) images, uniform labels, torchvision-style init",
+        "config": {"workload": f"{args.arch}@{args.image} training step, k*={k} per GPU "
+                   f"(bounded sample of {args.cpu_sample} images per timed step)",
+                   "cap_gib": args.cap_gib},
+        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads,
+                         "kind": "port", "sample": f"{args.cpu_sample} images/step, torch fp32 "
+                         "CPU restatement (oracle/resnet_torch.py)"},
+        "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1901_06773_b200 import planner, trainer
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    # ---- host side of the path: spec, profiles -> model, tuner -> plan, LR ----
+    network_json, desc = trainer.export_network(args.arch, args.image, args.classes, k_base=8)
+    link = {}
+    lp = os.path.join(ROOT, "profiles", "b200", "host_link.json")
+    if os.path.exists(lp):
+        link = json.load(open(lp))
+    pcie = float(link.get("d2h", 50.0)) * 1e9
+    m_others = trainer.default_m_others(desc, args.image)
+    hardware_json = trainer.hardware_json(int(args.cap_gib * GIB), m_others, pcie)
+    model_json, plan_json, plan_s, prof_src = plan_for(args, network_json, hardware_json)
+    plan = json.loads(plan_json)
+    k = plan["k_star"]
+    q = world * k / 8.0
+    lr, _, _ = planner.tune_lr(0.1, 1.0, max(1.0, q))
+
+    ex = trainer.Executor(args.arch, args.image, args.classes, mode="dynamic", plan_json=plan_json,
+                          network_json=network_json, hardware_json=hardware_json, device=local)
+    ex.set_params(trainer.init_params(desc, seed=0))
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(trainer.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ex.set_comm(uid.cpu().numpy().tobytes(), rank, world)
+    ex.set_graph(not args.no_graph)
+
+    g = np.random.default_rng(100 + rank)
+    x_host = torch.from_numpy(g.standard_normal((k, 3, args.image, args.image)).astype(np.float32)).pin_memory()
+    y_host = torch.from_numpy(g.integers(0, args.classes, size=k).astype(np.int32)).pin_memory()
+    x_dev, y_dev = x_host.to(dev), y_host.to(dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (first step captures the CUDA graph on the second call)
+    for _ in range(max(3, args.warmup)):
+        ex.step(x_dev, y_dev, lr=lr)
+
+    # ---- timed: device-resident inputs ----
+    barrier()
+    dev_ms = 0.0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            st = ex.step(x_dev, y_dev, lr=lr)
+            dev_ms += st["iter_ms"]
+    barrier()
+    ms_per_step = max_over_ranks(dev_ms / args.steps)
+    value = world * k / (ms_per_step * 1e-3)
+
+    # ---- timed: end to end with pinned host inputs ----
+    barrier()
+    t0 = time.perf_counter()
+    e2e_dev_ms = 0.0
+    for _ in range(args.steps):
+        st = ex.step(x_host, y_host, lr=lr)
+        e2e_dev_ms += st["iter_ms"]
+    barrier()
+    e2e_wall = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    e2e_value = world * k / e2e_wall
+
+    # ---- one profiled step (not timed): exposed swap + conv roofline ----
+    prof = ex.step(x_dev, y_dev, lr=lr, update=False, profile=True)
+    trace = ex.trace()
+    peaks = {}
+    pp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pp):
+        peaks = json.load(open(pp))
+    bf16 = float(peaks.get("bf16_tflops_sustained", 1405.3))
+    tf32_peak = round(bf16 / 2.0, 1)
+    roof = roofline_from_trace(desc, trace, k, tf32_peak, len(desc["ops"]))
+    roof["peak_note"] = ("TF32 dense peak taken as 1/2 of the measured cuBLAS bf16 sustained "
+                         "figure in MEASURED_PEAKS.json (nominal 1.1 vs 2.25 PF)")
+    arena, fixed = ex.memory()
+    f_conv = conv_flops_per_image(desc)
+    swapped = prof["swapped_bytes"]
+    t_conv = k * f_conv / (tf32_peak * 1e12)
+    t_swap = swapped / pcie if swapped else 0.0
+    img_roof = k / max(t_conv, t_swap)
+
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    try:
+        cpu_rate, cpu_dt = cpu_step_rate(args.arch, args.image, args.classes, args.cpu_sample,
+                                         threads)
+    except Exception as e:  # never fail the GPU line on the CPU baseline
+        cpu_rate, cpu_dt = None, str(e)
+    ref_plan_s = None
+    try:
+        ref_plan_s = reference_planner_seconds(network_json, hardware_json, model_json)
+    except Exception:
+        pass
+    clk = clocks.summary()
+    n_fm = len(desc["ops"])
+    line = {
+        "metric": "images/s (ResNet-152 training step, tuned minibatch, device cap)",
+        "value": round(value, 2), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TF32 tensor-core convolutions)",
+        "data": "synthetic N(0,1) 224x224 images, uniform labels, torchvision-style random init",
+        "config": {"workload": f"{args.arch}@{args.image}, {args.cap_gib:g} GiB device cap per GPU, "
+                   f"tuner k*={k} per GPU, global batch {world * k}",
+                   "model": args.arch, "global_batch": world * k, "k_star": k,
+                   "parallelism": f"dp{world}", "cap_bytes": int(args.cap_gib * GIB),
+                   "pinned_featuremaps": f"{len(plan['pinned_objects'])}/{n_fm}",
+                   "lr_alpha_star": lr, "cuda_graph": not args.no_graph,
+                   "l2": "inputs > L2: each step streams ~k*273 MiB of activations",
+                   "profiles": prof_src},
+        "e2e": {"value": round(e2e_value, 2), "unit": "images/s",
+                "h2d_bytes_per_step": int(x_host.numel() * 4 + y_host.numel() * 4),
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": kernel_launches_per_step(desc),
+        "roofline": roof,
+        "roofline_official": {"img_per_s_roof": round(img_roof * world, 2),
+                              "frac": round(value / (img_roof * world), 4),
+                              "definition": "k / max(k*F_conv/P_tf32, B_swap/BW_host) per GPU"},
+        "memory": {"peak_device_bytes": int(arena + fixed), "arena_bytes": int(arena),
+                   "fixed_bytes": int(fixed), "cap_bytes": int(args.cap_gib * GIB)},
+        "swap": {"swapped_bytes_per_step": int(swapped),
+                 "exposed_swap_ms": round(prof["exposed_swap_ms"], 3),
+                 "exposed_swap_frac": round(prof["exposed_swap_ms"] / max(prof["iter_ms"], 1e-9), 4)},
+        "planner": {"plan_seconds_b200_host": round(plan_s, 4),
+                    "reference_planner_seconds_step16": None if ref_plan_s is None else round(ref_plan_s, 3)},
+        "clocks": clk,
+        "cpu_baseline": {"value": None if cpu_rate is None else round(cpu_rate, 3),
+                         "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.cpu_sample} images, one torch fp32 CPU step "
+                                   f"({cpu_dt if isinstance(cpu_dt, str) else round(cpu_dt, 2)} s)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
