@@ -35,6 +35,8 @@ int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float*
  * 1 = 3xTF32 (hi/lo operand split, ~FP32 accuracy, 3x MMA work) */
 int accudnn_set_conv_math(int mode);
 int accudnn_get_conv_math(void);
+/* 1 = TMA-fed kernels where the shape allows (default), 0 = cp.async kernel only */
+int accudnn_set_conv_impl(int impl);
 /* splits <= 0 picks a split-K factor automatically (fp32 atomics) */
 int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,
                        float* dw, int beta, int splits, void* stream);

@@ -109,6 +109,7 @@ _F = ctypes.c_float
 CUDA_SYMBOLS = {
     "accudnn_set_conv_math": ([_I], _I),
     "accudnn_get_conv_math": ([], _I),
+    "accudnn_set_conv_impl": ([_I], _I),
     "accudnn_conv_fwd": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_dgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_wgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _I, _P], _I),

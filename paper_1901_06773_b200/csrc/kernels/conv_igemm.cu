@@ -481,6 +481,15 @@ int sm_count() {
 }
 
 }  // namespace
+
+// TMA-fed v2 kernels (conv_tma.cu); return 0 when a shape is not eligible
+int conv_tma_fwd(const accudnn_conv_desc* d, const float* x, const float* w, float* y, int beta,
+                 cudaStream_t st, int* rc);
+int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, float* dx,
+                   int beta, cudaStream_t st, int* rc);
+int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, float* dw,
+                   int beta, cudaStream_t st, int* rc);
+int g_conv_impl = 1;  // 1 = TMA kernels where eligible, 0 = cp.async kernel only
 }  // namespace accudnn
 
 using namespace accudnn;
@@ -489,6 +498,9 @@ extern "C" int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, cons
                                 float* y, int beta, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
+  int rc = 0;
+  if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_fwd(d, x, w, y, beta, stream, &rc))
+    return rc;
   Args a = make_args(d, FWD);
   a.a_src = x; a.b_src = w; a.out = y; a.beta = beta;
   return dispatch<FWD>(a, 1, stream);
@@ -498,6 +510,9 @@ extern "C" int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, c
                                   float* dx, int beta, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
+  int rc = 0;
+  if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_dgrad(d, dy, w, dx, beta, stream, &rc))
+    return rc;
   Args a = make_args(d, DGRAD);
   a.a_src = dy; a.b_src = w; a.out = dx; a.beta = beta;
   return dispatch<DGRAD>(a, 1, stream);
@@ -507,6 +522,10 @@ extern "C" int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, co
                                   float* dw, int beta, int splits, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
+  int rc = 0;
+  if (g_conv_impl == 1 && g_conv_math == 0 && splits <= 0 &&
+      conv_tma_wgrad(d, x, dy, dw, beta, stream, &rc))
+    return rc;
   Args a = make_args(d, WGRAD);
   a.a_src = dy; a.b_src = x; a.out = dw; a.beta = beta;
   if (splits <= 0) splits = pick_splits(a, sm_count());
@@ -524,3 +543,9 @@ extern "C" int accudnn_set_conv_math(int mode) {
   return 0;
 }
 extern "C" int accudnn_get_conv_math(void) { return accudnn::g_conv_math; }
+
+extern "C" int accudnn_set_conv_impl(int impl) {
+  if (impl != 0 && impl != 1) return static_cast<int>(cudaErrorInvalidValue);
+  accudnn::g_conv_impl = impl;
+  return 0;
+}

@@ -26,6 +26,15 @@ SHAPES = [
     (4, 256, 7, 7, 512, 3, 1, 1),
     (5, 2048, 1, 1, 1000, 1, 1, 0),   # fully connected
     (1, 36, 9, 9, 20, 3, 1, 1),       # ragged channel counts / tails
+    # TMA-path shapes (ResNet-152 stage geometry at small batch)
+    (4, 64, 56, 56, 64, 3, 1, 1),
+    (8, 256, 14, 14, 256, 3, 1, 1),
+    (4, 128, 28, 28, 128, 3, 2, 1),
+    (8, 256, 14, 14, 1024, 1, 1, 0),
+    (8, 1024, 14, 14, 256, 1, 1, 0),
+    (8, 512, 14, 14, 1024, 1, 2, 0),
+    (27, 2048, 1, 1, 1000, 1, 1, 0),
+    (3, 96, 10, 10, 160, 3, 1, 1),
 ]
 
 
@@ -46,8 +55,16 @@ def check(got, ref):
     assert (got - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-6
 
 
+@pytest.fixture(params=[1, 0], ids=["tma", "cpasync"])
+def impl(request):
+    lib = _native.cuda_lib()
+    lib.accudnn_set_conv_impl(request.param)
+    yield request.param
+    lib.accudnn_set_conv_impl(1)
+
+
 @pytest.mark.parametrize("shape", SHAPES)
-def test_conv_fwd_dgrad_wgrad(cuda_dev, shape):
+def test_conv_fwd_dgrad_wgrad(cuda_dev, impl, shape):
     lib = _native.cuda_lib()
     n, c, h, w, k, r, stride, pad = shape
     d, p, q = desc(*shape)
