@@ -38,6 +38,12 @@ void accudnn_rt_free(void* p);
 int accudnn_net_export(const char* arch, int image, int classes, int k_base, int lookahead,
                        char** network_json, char** describe_json);
 
+/* executor memory model without a GPU: peak live bytes of the real tensor
+ * instances and the static arena size for a swap mask (one char per op,
+ * nonzero = featuremap offloaded) at minibatch k */
+int accudnn_net_memory(const char* arch, int image, int classes, int k, int lookahead,
+                       const char* swapped_mask, long long* live_peak, long long* arena_bytes);
+
 /* mode: "resident" (nothing swapped), "naive" (every featuremap swapped) or
  * "dynamic" (plan_json's pinned_objects stay, the rest swap).  k = 0 takes
  * plan_json's k_star.  hardware_json (may be NULL) supplies the device cap

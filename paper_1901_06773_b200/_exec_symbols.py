@@ -19,6 +19,7 @@ SYMBOLS = {
     "accudnn_rt_last_error": ([], _S),
     "accudnn_rt_free": ([_P], None),
     "accudnn_net_export": ([_S, _I, _I, _I, _I, ctypes.POINTER(_P), ctypes.POINTER(_P)], _I),
+    "accudnn_net_memory": ([_S, _I, _I, _I, _I, _P, ctypes.POINTER(_LL), ctypes.POINTER(_LL)], _I),
     "accudnn_exec_create": ([_S, _I, _I, _S, _S, _S, _S, _I, _I, _I, ctypes.POINTER(_P)], _I),
     "accudnn_exec_destroy": ([_P], _I),
     "accudnn_exec_num_params": ([_P], _LL),

@@ -64,6 +64,21 @@ int accudnn_net_export(const char* arch, int image, int classes, int k_base, int
   });
 }
 
+int accudnn_net_memory(const char* arch, int image, int classes, int k, int lookahead,
+                       const char* swapped_mask, long long* live_peak, long long* arena_bytes) {
+  return guarded([&] {
+    const accudnn::Net net = accudnn::build_net(arch, image, classes);
+    std::vector<char> sw(static_cast<size_t>(net.num_ops()), 0);
+    if (swapped_mask)
+      for (int i = 0; i < net.num_ops(); ++i) sw[static_cast<size_t>(i)] = swapped_mask[i] != 0;
+    accudnn::LifetimeModel lm = accudnn::build_lifetimes(net, k, sw, lookahead, 512);
+    if (live_peak) *live_peak = lm.peak_bytes;
+    const long long arena = accudnn::plan_arena(lm);
+    if (arena_bytes) *arena_bytes = arena;
+    return 0;
+  });
+}
+
 int accudnn_exec_create(const char* arch, int image, int classes, const char* mode,
                         const char* network_json, const char* hardware_json,
                         const char* plan_json, int k, int device, int lookahead,

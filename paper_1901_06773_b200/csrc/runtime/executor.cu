@@ -85,34 +85,7 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
 
   // ---- static arena plan ----
   I.lm = build_lifetimes(net_, cfg.k, I.swapped, cfg.lookahead, kAlign);
-  std::vector<int> order(I.lm.inst.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    const Instance& x = I.lm.inst[static_cast<size_t>(a)];
-    const Instance& y = I.lm.inst[static_cast<size_t>(b)];
-    if (x.bytes != y.bytes) return x.bytes > y.bytes;
-    return x.first < y.first;
-  });
-  std::vector<int> placed;
-  long long arena = 0;
-  for (int id : order) {
-    Instance& x = I.lm.inst[static_cast<size_t>(id)];
-    // occupied ranges of time-overlapping placed instances, sorted by offset
-    std::vector<std::pair<long long, long long>> busy;
-    for (int p : placed) {
-      const Instance& y = I.lm.inst[static_cast<size_t>(p)];
-      if (y.first <= x.last && x.first <= y.last) busy.emplace_back(y.offset, y.offset + y.bytes);
-    }
-    std::sort(busy.begin(), busy.end());
-    long long off = 0;
-    for (const auto& [lo, hi] : busy) {
-      if (off + x.bytes <= lo) break;
-      off = std::max(off, hi);
-    }
-    x.offset = off;
-    arena = std::max(arena, off + x.bytes);
-    placed.push_back(id);
-  }
+  const long long arena = plan_arena(I.lm);
   arena_bytes_ = static_cast<unsigned long long>(arena);
 
   // region predecessors: earlier (in time) instances sharing bytes

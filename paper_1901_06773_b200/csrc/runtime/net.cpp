@@ -526,6 +526,37 @@ LifetimeModel build_lifetimes(const Net& net, int k, const std::vector<char>& sw
   return lm;
 }
 
+long long plan_arena(LifetimeModel& lm) {
+  std::vector<int> order(lm.inst.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const Instance& x = lm.inst[static_cast<size_t>(a)];
+    const Instance& y = lm.inst[static_cast<size_t>(b)];
+    if (x.bytes != y.bytes) return x.bytes > y.bytes;
+    return x.first < y.first;
+  });
+  std::vector<int> placed;
+  long long arena = 0;
+  for (int id : order) {
+    Instance& x = lm.inst[static_cast<size_t>(id)];
+    std::vector<std::pair<long long, long long>> busy;
+    for (int p : placed) {
+      const Instance& y = lm.inst[static_cast<size_t>(p)];
+      if (y.first <= x.last && x.first <= y.last) busy.emplace_back(y.offset, y.offset + y.bytes);
+    }
+    std::sort(busy.begin(), busy.end());
+    long long off = 0;
+    for (const auto& [lo, hi] : busy) {
+      if (off + x.bytes <= lo) break;
+      off = std::max(off, hi);
+    }
+    x.offset = off;
+    arena = std::max(arena, off + x.bytes);
+    placed.push_back(id);
+  }
+  return arena;
+}
+
 // ---------------------------------------------------------------------------
 // exporter
 // ---------------------------------------------------------------------------

@@ -104,6 +104,10 @@ struct LifetimeModel {
 LifetimeModel build_lifetimes(const Net& net, int k, const std::vector<char>& swapped,
                               int lookahead, long long align);
 
+// static arena offsets: greedy by size, first fit against time-overlapping
+// instances; returns the arena size in bytes
+long long plan_arena(LifetimeModel& lm);
+
 // reference-format network.json (format_version 1) with k_base images
 std::string export_network_json(const Net& net, int k_base, int lookahead);
 // layer <-> op description for host tooling and the torch oracle

@@ -50,6 +50,17 @@ def export_network(arch, image, classes, k_base=8, lookahead=1):
     return _take(a.value), json.loads(_take(b.value))
 
 
+def net_memory(arch, image, classes, k, swapped, lookahead=1):
+    """(peak live bytes, static arena bytes) of the executor's tensor
+    instances for a swap mask -- computed on the host, no GPU needed."""
+    mask = (ctypes.c_char * len(swapped))(*[b"\x01" if s else b"\x00" for s in swapped])
+    live, arena = ctypes.c_longlong(), ctypes.c_longlong()
+    _check(_lib().accudnn_net_memory(arch.encode(), int(image), int(classes), int(k),
+                                     int(lookahead), mask, ctypes.byref(live),
+                                     ctypes.byref(arena)), "net memory")
+    return live.value, arena.value
+
+
 def hardware_json(budget_bytes, m_others_bytes, pcie_bytes_per_s, delta_sync_s=0.0):
     return json.dumps({"format_version": 1, "memory_budget_bytes": int(budget_bytes),
                        "m_others_bytes": int(m_others_bytes), "delta_sync_s": float(delta_sync_s),

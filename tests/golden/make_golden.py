@@ -1,0 +1,117 @@
+"""Generates tests/golden/*.json from the compiled REFERENCE planner
+(oracle/_ref/libswapsched_ref.so, built from /root/reference/proj/src by
+oracle/Makefile).  Test infrastructure: run here, commit the outputs; the
+tests then pin the B200 planner against them without the reference tree.
+
+  planner_fixtures.json  for seeds of the reference's fixture generator
+                         (synthetic.cpp:170-195): the four input documents'
+                         digests, model.json, plan.json, evaluate_minibatch at
+                         k*, k*+1, k_max, simulate(dynamic) summary + trace
+                         FNV-1a, sweep CSV
+  resnet_plans.json      exported ResNet network.json + B200 profiles ->
+                         per-k evaluations and small-budget full plans
+"""
+import ctypes
+import hashlib
+import json
+import os
+import struct
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from paper_1901_06773_b200 import _native, planner  # noqa: E402
+
+SEEDS = [1, 5, 7, 42, 99, 3, 11, 23, 64, 77, 101, 202, 303, 404, 505, 606]
+
+
+def fnv1a(data):
+    h = 1469598103934665603
+    for c in data:
+        h ^= c
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return "%016x" % h
+
+
+def t_ready_digest(ns):
+    return fnv1a(struct.pack("<%dq" % len(ns), *ns))
+
+
+def ref_lib():
+    lib = ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libswapsched_ref.so"))
+    _native.declare_planner_symbols(lib, "oracle_")
+    return dict(lib=lib, prefix="oracle_")
+
+
+def fixture_record(seed, R):
+    fx = planner.generate_fixture(seed, **R)
+    model = planner.fit(fx["network"], [fx["compute_csv"], fx["transfer_csv"]], fx["hardware"], **R)
+    rec = {"seed": seed,
+           "docs_sha256": {k: hashlib.sha256(v.encode()).hexdigest() for k, v in fx.items()},
+           "model_json": model, "k_max": planner.kmax(fx["network"], fx["hardware"], **R)}
+    try:
+        plan = planner.plan(fx["network"], fx["hardware"], model, **R)
+        rec["plan_json"] = plan
+        k = json.loads(plan)["k_star"]
+        evals = {}
+        for kk in sorted({1, k, k + 1, rec["k_max"]}):
+            evals[str(kk)] = planner.evaluate_k(fx["network"], fx["hardware"], model, kk, **R)
+        rec["evals"] = evals
+        rec["t_ready_fnv1a"] = t_ready_digest(evals[str(k)]["t_ready_ns"])
+        sims = {}
+        for mode in ("naive", "dynamic", "resident"):
+            rc, summ, trace = planner.simulate(fx["network"], fx["hardware"], model, plan, mode, k, **R)
+            sims[mode] = {"rc": rc, "summary": summ, "trace_fnv1a": fnv1a(trace.encode())}
+        rec["sim"] = sims
+        rec["sweep_csv"] = planner.sweep(fx["network"], fx["hardware"], model,
+                                         sorted({1, max(1, k // 2), k, k + 1}), **R)
+    except planner.PlannerError as e:
+        rec["plan_error"] = {"code": e.code, "document": e.document}
+    return rec
+
+
+def resnet_records(R):
+    from paper_1901_06773_b200 import trainer
+    out = []
+    cases = [("resnet20", 32, 12, 64 << 20, "resnet20"), ("resnet50", 224, 1000, 12 << 30, "resnet50"),
+             ("resnet152", 224, 1000, 8 << 30, "resnet152")]
+    link = json.load(open(os.path.join(ROOT, "profiles", "b200", "host_link.json")))
+    for arch, image, classes, budget, prof in cases:
+        net, desc = trainer.export_network(arch, image, classes, k_base=8)
+        hw = trainer.hardware_json(budget, trainer.default_m_others(desc, image), link["d2h"] * 1e9)
+        pdir = os.path.join(ROOT, "profiles", "b200")
+        csvs = []
+        for kind in ("compute", "transfer"):
+            p = os.path.join(pdir, f"{prof}_{kind}_profile.csv")
+            if os.path.exists(p):
+                csvs.append(open(p).read())
+        if len(csvs) < 2:  # no measured profile: flat B200-like synthetic curves
+            continue
+        model = planner.fit(net, csvs, hw, **R)
+        km = planner.kmax(net, hw, **R)
+        rec = {"arch": arch, "image": image, "classes": classes, "budget": budget,
+               "network_sha256": hashlib.sha256(net.encode()).hexdigest(), "model_json": model,
+               "hardware_json": hw, "k_max": km, "evals": {}}
+        for kk in (1, 8, 16, 24, 27, 32, 48, 64):
+            if kk <= km:
+                rec["evals"][str(kk)] = planner.evaluate_k(net, hw, model, kk, **R)
+        if arch == "resnet20":
+            rec["plan_json"] = planner.plan(net, hw, model, **R)
+        out.append(rec)
+    return out
+
+
+def main():
+    R = ref_lib()
+    fixtures = [fixture_record(s, R) for s in SEEDS]
+    with open(os.path.join(HERE, "planner_fixtures.json"), "w") as f:
+        json.dump(fixtures, f, indent=1)
+    with open(os.path.join(HERE, "resnet_plans.json"), "w") as f:
+        json.dump(resnet_records(R), f, indent=1)
+    print("wrote", len(fixtures), "fixtures")
+
+
+if __name__ == "__main__":
+    main()
