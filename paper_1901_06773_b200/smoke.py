@@ -25,13 +25,23 @@ def run():
     y = g.integers(0, classes, size=k).astype(np.int32)
     out = ex.step(x, y, lr=0.0, update=False)
     grads = ex.get_grads()
-    loss, g_ref, _, _ = TorchResNet(desc).step(params, torch.zeros(desc["n_stats"]), None, x, y,
-                                               lr=0.0, update=False)
-    rel_loss = abs(out["loss"] - loss) / abs(loss)
-    rel_g = float(np.linalg.norm(grads - g_ref) / np.linalg.norm(g_ref))
-    print(f"smoke: loss {out['loss']:.6f} (oracle {loss:.6f}, rel {rel_loss:.2e}), "
-          f"grad rel-L2 {rel_g:.2e}, swapped {out['swapped_bytes']} B")
-    assert rel_loss < 2e-3 and rel_g < 2e-2
+    # the convolutions run on TF32 tensor cores: the device step must be as
+    # close to the float64 ground truth as an fp32 step whose convolutions see
+    # TF32-truncated operands (within 3x, or 2e-3) -- the tolerance of
+    # tests/test_train_step_gpu.py::test_step_tf32_mode_matches_tf32_oracle
+    def oracle(dtype, conv_math):
+        loss, g, _, _ = TorchResNet(desc, dtype, conv_math).step(
+            params, torch.zeros(desc["n_stats"]), None, x, y, lr=0.0, update=False)
+        return loss, np.asarray(g, np.float64)
+    l64, g64 = oracle(torch.float64, "exact")
+    lt, gt = oracle(torch.float32, "tf32")
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    e_l, e_lt = abs(out["loss"] - l64) / abs(l64), abs(lt - l64) / abs(l64)
+    e_g, e_gt = rel(grads, g64), rel(gt, g64)
+    print(f"smoke: loss {out['loss']:.6f} (fp64 oracle {l64:.6f}); loss err {e_l:.2e} "
+          f"(tf32 oracle {e_lt:.2e}); grad rel-L2 err {e_g:.2e} (tf32 oracle {e_gt:.2e}); "
+          f"swapped {out['swapped_bytes']} B")
+    assert e_l <= max(3 * e_lt, 2e-3) and e_g <= max(3 * e_gt, 2e-3)
 
 
 if __name__ == "__main__":

@@ -1,4 +1,6 @@
-"""Times the tcgen05 conv kernels on representative ResNet-152 shapes (k=24)."""
+"""Times the tcgen05 conv kernels on every distinct ResNet-152 conv shape at
+k images (default 27 = the tuner's k* at 8 GiB) next to cuDNN TF32 (torch,
+channels_last) as a yardstick.  Usage: conv_bench.py [k] [json_out]"""
 import ctypes
 import json
 import sys
@@ -6,52 +8,83 @@ import sys
 import torch
 
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
-from paper_1901_06773_b200 import _native  # noqa: E402
+from paper_1901_06773_b200 import _native, trainer  # noqa: E402
 
-SHAPES = {
-    "s1_conv2_3x3": (24, 64, 56, 56, 64, 3, 1, 1),
-    "s1_conv3_1x1": (24, 64, 56, 56, 256, 1, 1, 0),
-    "s3_conv1_1x1": (24, 1024, 14, 14, 256, 1, 1, 0),
-    "s3_conv2_3x3": (24, 256, 14, 14, 256, 3, 1, 1),
-    "s3_conv3_1x1": (24, 256, 14, 14, 1024, 1, 1, 0),
-    "s4_conv2_3x3": (24, 512, 7, 7, 512, 3, 1, 1),
-    "stem_7x7": (24, 4, 224, 224, 64, 7, 2, 3),
-}
+
+def shapes(k):
+    _, d = trainer.export_network("resnet152", 224, 1000)
+    ops = d["ops"]
+    seen = {}
+    for o in ops:
+        if o["kind"] != "conv":
+            continue
+        src = ops[o["in0"]]["out"] if o["in0"] >= 0 else [224, 224, 4]
+        key = (k, o["cin"] if o["in0"] >= 0 else 4, src[0], src[1], o["cout"], o["r"], o["stride"], o["pad"])
+        seen[key] = seen.get(key, 0) + 1
+    return seen
+
+
+def timeit(fn, iters=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
 
 
 def main():
+    k = int(sys.argv[1]) if len(sys.argv) > 1 else 27
     lib = _native.cuda_lib()
     dev = torch.device("cuda:0")
-    out = {}
-    for name, (n, c, h, w, k, r, st, pad) in SHAPES.items():
+    torch.backends.cudnn.allow_tf32 = True
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.benchmark = True
+    out = []
+    tot = {"ours": 0.0, "cudnn": 0.0, "gflop": 0.0}
+    for (n, c, h, w, kk, r, st, pad), count in shapes(k).items():
         p = (h + 2 * pad - r) // st + 1
         q = (w + 2 * pad - r) // st + 1
-        d = _native.ConvDesc(n, h, w, c, k, r, r, st, pad, p, q)
+        d = _native.ConvDesc(n, h, w, c, kk, r, r, st, pad, p, q)
         x = torch.randn(n, h, w, c, device=dev)
-        wt = torch.randn(k, r, r, c, device=dev) * 0.01
-        y = torch.empty(n, p, q, k, device=dev)
-        dy = torch.randn(n, p, q, k, device=dev)
+        wt = torch.randn(kk, r, r, c, device=dev) * 0.01
+        y = torch.empty(n, p, q, kk, device=dev)
+        dy = torch.randn(n, p, q, kk, device=dev)
         dx = torch.empty_like(x)
         dw = torch.empty_like(wt)
-        flops = 2.0 * n * p * q * k * c * r * r
-        res = {}
-        for mode, fn in (("fwd", lambda: lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), wt.data_ptr(), y.data_ptr(), 0, None)),
-                         ("dgrad", lambda: lib.accudnn_conv_dgrad(ctypes.byref(d), dy.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, None)),
-                         ("wgrad", lambda: lib.accudnn_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, 0, None))):
-            for _ in range(3):
-                fn()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            iters = 20
-            a.record()
-            for _ in range(iters):
-                fn()
-            b.record()
-            torch.cuda.synchronize()
-            ms = a.elapsed_time(b) / iters
-            res[mode] = {"ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1)}
-        out[name] = res
-        print(name, json.dumps(res), flush=True)
+        flops = 2.0 * n * p * q * kk * c * r * r
+        # cuDNN yardstick (NCHW logical view of the NHWC buffers = channels_last)
+        xc = x.permute(0, 3, 1, 2)
+        wc = wt.permute(0, 3, 1, 2)
+        dyc = dy.permute(0, 3, 1, 2)
+        res = {"shape": f"{h}x{w} {c}->{kk} r{r} s{st}", "count": count}
+        for mode, fn, cfn in (
+            ("fwd", lambda: lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), wt.data_ptr(), y.data_ptr(), 0, None),
+             lambda: torch.nn.functional.conv2d(xc, wc, stride=st, padding=pad)),
+            ("dgrad", lambda: lib.accudnn_conv_dgrad(ctypes.byref(d), dy.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, None),
+             lambda: torch.ops.aten.convolution_backward(dyc, xc, wc, None, [st, st], [pad, pad], [1, 1], False, [0, 0], 1, [True, False, False])),
+            ("wgrad", lambda: lib.accudnn_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, 0, None),
+             lambda: torch.ops.aten.convolution_backward(dyc, xc, wc, None, [st, st], [pad, pad], [1, 1], False, [0, 0], 1, [False, True, False]))):
+            if mode == "dgrad" and x.shape[-1] == 4:
+                continue
+            ms = timeit(fn)
+            cms = timeit(cfn)
+            res[mode] = {"ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1),
+                         "cudnn_ms": round(cms, 4), "cudnn_tflops": round(flops / cms / 1e9, 1)}
+            tot["ours"] += ms * count
+            tot["cudnn"] += cms * count
+            tot["gflop"] += flops * count / 1e9
+        out.append(res)
+        print(json.dumps(res), flush=True)
+    tot["ours_tflops"] = round(tot["gflop"] / tot["ours"], 1)
+    tot["cudnn_tflops"] = round(tot["gflop"] / tot["cudnn"], 1)
+    print("TOTAL", json.dumps(tot), flush=True)
+    if len(sys.argv) > 2:
+        json.dump({"k": k, "shapes": out, "total": tot}, open(sys.argv[2], "w"), indent=1)
 
 
 if __name__ == "__main__":
