@@ -37,7 +37,13 @@ int accudnn_set_conv_math(int mode);
 int accudnn_get_conv_math(void);
 /* 1 = TMA-fed kernels where the shape allows (default), 0 = cp.async kernel only */
 int accudnn_set_conv_impl(int impl);
-/* splits <= 0 picks a split-K factor automatically (fp32 atomics) */
+/* split-K workspace of the persistent TMA kernels (deterministic fix-up:
+ * partials are summed in slice order).  ptr == NULL: bytes > 0 restores a
+ * lazily allocated default of that size (64 MiB initially), bytes == 0
+ * disables split-K.  Splits are limited so that splits * M * N * 4 <= bytes. */
+int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes);
+/* splits <= 0 picks a split-K factor automatically (TMA path: deterministic
+ * workspace fix-up; cp.async fallback: fp32 atomics) */
 int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,
                        float* dw, int beta, int splits, void* stream);
 

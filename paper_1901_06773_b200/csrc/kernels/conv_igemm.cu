@@ -482,7 +482,7 @@ int sm_count() {
 
 }  // namespace
 
-// TMA-fed v2 kernels (conv_tma.cu); return 0 when a shape is not eligible
+// persistent TMA kernels (conv_sm100.cu); return 0 when a shape is not eligible
 int conv_tma_fwd(const accudnn_conv_desc* d, const float* x, const float* w, float* y, int beta,
                  cudaStream_t st, int* rc);
 int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, float* dx,

@@ -47,6 +47,7 @@ struct Executor::Impl {
   int* labels = nullptr;
   float* loss = nullptr;
   float* loss_host = nullptr;    // pinned
+  void* conv_ws = nullptr;       // split-K partials of the conv kernels
   std::vector<float*> host_store;  // pinned host copies of swapped featuremaps
   // streams / events
   cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr, comm_stream = nullptr;
@@ -120,6 +121,18 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   const size_t img4 = sizeof(float) * static_cast<size_t>(k) * cfg.image * cfg.image * net_.in_c4;
   const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg.image * cfg.image * net_.in_c;
   fixed_bytes_ = 3 * pbytes + sbytes + wsbytes + img4 + img3 + sizeof(int) * k + 256;
+  // split-K workspace of the convolutions: whatever the planner's fixed
+  // allowance leaves, capped at 64 MiB; the kernels pick their split
+  // factors to fit it
+  size_t conv_ws = 64u << 20;
+  if (cfg.budget && cfg.fixed_allowance) {
+    const unsigned long long used = fixed_bytes_;
+    conv_ws = used >= cfg.fixed_allowance
+                  ? 0
+                  : std::min<size_t>(conv_ws, static_cast<size_t>(cfg.fixed_allowance - used));
+    conv_ws &= ~static_cast<size_t>(4095);
+  }
+  fixed_bytes_ += conv_ws;
   if (cfg.budget) {
     if (cfg.fixed_allowance && fixed_bytes_ > cfg.fixed_allowance)
       throw std::runtime_error("fixed device allocations (" + std::to_string(fixed_bytes_) +
@@ -141,6 +154,8 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaMalloc(&I.labels, sizeof(int) * k), "labels");
   ck(cudaMalloc(&I.loss, 256), "loss");
   ck(cudaMallocHost(&I.loss_host, sizeof(float)), "loss host");
+  if (conv_ws) ck(cudaMalloc(&I.conv_ws, conv_ws), "conv workspace");
+  ckl(accudnn_conv_set_workspace(I.conv_ws, I.conv_ws ? conv_ws : 0), "conv workspace");
   ck(cudaMemset(I.params, 0, pbytes), "memset");
   ck(cudaMemset(I.grads, 0, pbytes), "memset");
   ck(cudaMemset(I.momentum_buf, 0, pbytes), "memset");
@@ -202,8 +217,9 @@ Executor::~Executor() {
                   static_cast<void*>(I.grads), static_cast<void*>(I.momentum_buf),
                   static_cast<void*>(I.stats), I.bn_ws, static_cast<void*>(I.image),
                   static_cast<void*>(I.image_nchw), static_cast<void*>(I.labels),
-                  static_cast<void*>(I.loss)})
+                  static_cast<void*>(I.loss), I.conv_ws})
     if (p) cudaFree(p);
+  if (I.conv_ws || cfg_.budget) accudnn_conv_set_workspace(nullptr, 64ull << 20);
 }
 
 void Executor::set_params(const float* host, long long n) {

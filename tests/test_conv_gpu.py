@@ -35,6 +35,14 @@ SHAPES = [
     (8, 512, 14, 14, 1024, 1, 2, 0),
     (27, 2048, 1, 1, 1000, 1, 1, 0),
     (3, 96, 10, 10, 160, 3, 1, 1),
+    # stride-2 data gradients (parity-class decomposition), odd and even sizes
+    (4, 64, 16, 16, 64, 3, 2, 1),
+    (2, 32, 7, 9, 64, 3, 2, 1),
+    (2, 64, 12, 12, 32, 1, 2, 0),
+    (3, 32, 11, 11, 64, 5, 2, 2),
+    # split-K heavy (small M, long K): ResNet-152 stage 3/4 at k* = 27
+    (27, 1024, 7, 7, 256, 1, 1, 0),
+    (27, 256, 14, 14, 256, 3, 1, 1),
 ]
 
 
@@ -112,3 +120,81 @@ def test_conv_accumulate_beta(cuda_dev):
     assert lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), w.data_ptr(), y1.data_ptr(), 0, None) == 0
     torch.cuda.synchronize()
     assert torch.allclose(y, y0 + y1, rtol=1e-5, atol=1e-5)
+
+
+def _run_all(lib, d, x_d, w_d, dy_d, outs):
+    y_d, dx_d, dw_d = outs
+    assert lib.accudnn_conv_fwd(ctypes.byref(d), x_d.data_ptr(), w_d.data_ptr(),
+                                y_d.data_ptr(), 0, None) == 0
+    assert lib.accudnn_conv_dgrad(ctypes.byref(d), dy_d.data_ptr(), w_d.data_ptr(),
+                                  dx_d.data_ptr(), 0, None) == 0
+    assert lib.accudnn_conv_wgrad(ctypes.byref(d), x_d.data_ptr(), dy_d.data_ptr(),
+                                  dw_d.data_ptr(), 0, 0, None) == 0
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shape", [(27, 1024, 14, 14, 256, 1, 1, 0), (27, 256, 14, 14, 256, 3, 1, 1),
+                                   (27, 512, 14, 14, 512, 3, 2, 1), (27, 2048, 7, 7, 512, 1, 1, 0)])
+def test_conv_bitwise_deterministic(cuda_dev, shape):
+    """split-K partials are reduced in slice order: repeated launches (and
+    launches after unrelated work reorders the SM schedule) are bit-identical."""
+    lib = _native.cuda_lib()
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    g = torch.Generator(device=cuda_dev).manual_seed(1)
+    x_d = torch.randn(n, h, w, c, device=cuda_dev, generator=g)
+    w_d = torch.randn(k, r, r, c, device=cuda_dev, generator=g) * 0.05
+    dy_d = torch.randn(n, p, q, k, device=cuda_dev, generator=g)
+    a = (torch.empty(n, p, q, k, device=cuda_dev), torch.empty(n, h, w, c, device=cuda_dev),
+         torch.empty(k, r, r, c, device=cuda_dev))
+    b = tuple(torch.empty_like(t) for t in a)
+    _run_all(lib, d, x_d, w_d, dy_d, a)
+    for _ in range(3):
+        torch.randn(1 << 22, device=cuda_dev).sum()  # perturb the schedule
+        _run_all(lib, d, x_d, w_d, dy_d, b)
+        for u, v in zip(a, b):
+            assert torch.equal(u, v)
+
+
+def test_conv_small_workspace_limits_splits(cuda_dev):
+    """a workspace too small for any split falls back to one K-slice per
+    tile and still computes the same convolution."""
+    lib = _native.cuda_lib()
+    shape = (27, 1024, 7, 7, 256, 1, 1, 0)
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    x_d = torch.randn(n, h, w, c, device=cuda_dev)
+    w_d = torch.randn(k, r, r, c, device=cuda_dev) * 0.03
+    dy_d = torch.randn(n, p, q, k, device=cuda_dev)
+    a = (torch.empty(n, p, q, k, device=cuda_dev), torch.empty(n, h, w, c, device=cuda_dev),
+         torch.empty(k, r, r, c, device=cuda_dev))
+    b = tuple(torch.empty_like(t) for t in a)
+    _run_all(lib, d, x_d, w_d, dy_d, a)
+    try:
+        assert lib.accudnn_conv_set_workspace(None, 0) == 0  # split-K disabled
+        _run_all(lib, d, x_d, w_d, dy_d, b)
+    finally:
+        lib.accudnn_conv_set_workspace(None, 64 << 20)
+    for u, v in zip(a, b):
+        assert rel_err(u.double(), v.double()) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 64, 1, 2, 0), (2, 64, 10, 10, 64, 3, 2, 1)])
+def test_dgrad_strided_accumulate(cuda_dev, shape):
+    """beta = 1 adds the stride-2 data gradient onto an existing one (the
+    block input of a ResNet downsample receives two gradient contributions)."""
+    lib = _native.cuda_lib()
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    w_d = torch.randn(k, r, r, c, device=cuda_dev) * 0.05
+    dy_d = torch.randn(n, p, q, k, device=cuda_dev)
+    base = torch.randn(n, h, w, c, device=cuda_dev)
+    acc = base.clone()
+    fresh = torch.full_like(base, float("nan"))
+    assert lib.accudnn_conv_dgrad(ctypes.byref(d), dy_d.data_ptr(), w_d.data_ptr(),
+                                  acc.data_ptr(), 1, None) == 0
+    assert lib.accudnn_conv_dgrad(ctypes.byref(d), dy_d.data_ptr(), w_d.data_ptr(),
+                                  fresh.data_ptr(), 0, None) == 0
+    torch.cuda.synchronize()
+    assert not torch.isnan(fresh).any()
+    assert torch.allclose(acc, base + fresh, rtol=1e-5, atol=1e-5)
