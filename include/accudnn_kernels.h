@@ -48,7 +48,9 @@ int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* 
                        float* dw, int beta, int splits, void* stream);
 
 /* batch normalisation over the M = n*h*w rows of an [M][C] tensor, training
- * mode; optional fused ReLU.  `ws` needs accudnn_bn_workspace_bytes(C). */
+ * mode; optional fused ReLU.  `ws` needs accudnn_bn_workspace_bytes(C) bytes,
+ * zeroed once before first use (the reductions keep their arrival counters
+ * there and re-arm them); one workspace per stream. */
 unsigned long long accudnn_bn_workspace_bytes(int C);
 int accudnn_bn_fwd(const float* x, long long M, int C, const float* gamma,
                    const float* beta, float eps, int relu, float* y,

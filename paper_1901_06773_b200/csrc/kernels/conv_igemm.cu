@@ -35,6 +35,10 @@
 #include "sm100_ptx.cuh"
 
 namespace accudnn {
+// split-K workspace + slice-order reduction (conv_sm100.cu)
+float* conv_splitk_workspace(size_t bytes);
+int conv_splitk_reduce(float* ws, int splits, int M, int Ng, float* out, int beta,
+                       cudaStream_t st);
 namespace {
 
 constexpr int kBM = 128;        // rows per tile (UMMA M)
@@ -54,7 +58,8 @@ struct Args {
   const float* b_src;  // FWD: w   DGRAD: w   WGRAD: x
   float* out;
   int beta;            // 1: accumulate into out
-  int atomic;          // split-K partial sums
+  int atomic;          // split-K partial sums (fp32 atomics into out)
+  float* ws;           // split-K partials [split][M][Ng] (deterministic), or nullptr
   int mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes, 0 = derived)
   int mn_layout;       // MN-major descriptor layout type (1 = SW128_BASE32B)
   int mn_kstep;        // debug override of the per-K=8 start advance
@@ -329,13 +334,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
         ptx::tmem_ld32(trow + c0, v);
         if (m < a.M) {
-          float* dst = a.out + static_cast<long long>(m) * a.Ng + n0 + c0;
+          float* dst = (a.ws ? a.ws + static_cast<long long>(blockIdx.z) * a.M * a.Ng : a.out) +
+                       static_cast<long long>(m) * a.Ng + n0 + c0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (n0 + c0 + 4 * g >= a.Ng) break;
             float4 o = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
             float4* d4 = reinterpret_cast<float4*>(dst + 4 * g);
-            if (a.atomic) {
+            if (a.ws) {
+              __stcg(d4, o);
+            } else if (a.atomic) {
               atomicAdd(&d4->x, o.x);
               atomicAdd(&d4->y, o.y);
               atomicAdd(&d4->z, o.z);
@@ -450,6 +458,22 @@ int dispatch(Args a, int splits, cudaStream_t stream) {
   a.kb_per_split = (a.kb_total + splits - 1) / splits;
   splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
   a.atomic = splits > 1 ? 1 : 0;
+  a.ws = nullptr;
+  if (splits > 1) {  // deterministic slice-order reduction when the workspace allows
+    a.ws = conv_splitk_workspace(sizeof(float) * static_cast<size_t>(splits) * a.M * a.Ng);
+    if (a.ws) {
+      a.atomic = 0;
+      int rc;
+      if (g_conv_math == 1)
+        rc = a.Ng <= 64 ? launch<MODE, 64, true>(a, splits, stream)
+                        : launch<MODE, 128, true>(a, splits, stream);
+      else
+        rc = a.Ng <= 64 ? launch<MODE, 64, false>(a, splits, stream)
+                        : launch<MODE, 128, false>(a, splits, stream);
+      if (rc) return rc;
+      return conv_splitk_reduce(a.ws, splits, a.M, a.Ng, a.out, a.beta, stream);
+    }
+  }
   if (g_conv_math == 1) {
     if (a.Ng <= 64) return launch<MODE, 64, true>(a, splits, stream);
     return launch<MODE, 128, true>(a, splits, stream);
@@ -529,7 +553,8 @@ extern "C" int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, co
   Args a = make_args(d, WGRAD);
   a.a_src = dy; a.b_src = x; a.out = dw; a.beta = beta;
   if (splits <= 0) splits = pick_splits(a, sm_count());
-  if (splits > 1 && !beta) {
+  if (splits > 1 && !beta &&
+      !conv_splitk_workspace(sizeof(float) * static_cast<size_t>(splits) * a.M * a.Ng)) {
     const cudaError_t e = cudaMemsetAsync(dw, 0, sizeof(float) * static_cast<size_t>(a.M) * a.Ng,
                                           stream);
     if (e != cudaSuccess) return static_cast<int>(e);

@@ -736,6 +736,26 @@ int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, 
   return 1;
 }
 
+// shared with the cp.async kernel (conv_igemm.cu): the split-K workspace if
+// it holds `bytes`, else nullptr; and the slice-order reduction on it
+float* conv_splitk_workspace(size_t bytes) {
+  return ws_capacity() >= bytes ? g_ws.ws : nullptr;
+}
+int conv_splitk_reduce(float* ws, int splits, int M, int Ng, float* out, int beta,
+                       cudaStream_t st) {
+  Prob a{};
+  a.ws = ws;
+  a.splits = splits;
+  a.M = M;
+  a.Ng = Ng;
+  a.out = out;
+  a.beta = beta;
+  const long long vec = static_cast<long long>(M) * (Ng / 4);
+  const int rgrid = static_cast<int>(std::min<long long>((vec + 255) / 256, 8LL * sm_count()));
+  conv_splitk_reduce_kernel<<<rgrid, 256, 0, st>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace accudnn
 
 // caller-provided split-K workspace (e.g. carved out of an executor's fixed

@@ -30,76 +30,123 @@ int grid_for(long long work, int per_block, int cap = 148 * 16) {
 // ---------------------------------------------------------------------------
 // batch normalisation
 // ---------------------------------------------------------------------------
-// Workspace layout (doubles): [0,C) sum  [C,2C) sum of squares / sum(dy*xhat)
-// then floats: [scale C][shift C]
+// Per-channel reductions are deterministic (no atomics on data): the grid is
+// (channel groups of <= 128 channels) x (Y row splits); every block writes
+// its partial sums to its own slot part[y][2][128-channel group], and the last
+// block of each channel group (arrival counter, re-armed by that block)
+// sums the Y slots in slot order in double precision and finalises:
+//   mode 0 (forward):  mean, invstd, scale = gamma*invstd, shift, running stats
+//   mode 1 (backward): s1 = sum g, s2 = sum g*xhat (g = dy * relu mask) ->
+//                      dbeta, dgamma and the two sums for the dx kernel.
+// Workspace layout: counters (uint) [kBnMaxGroups] | part (float)
+//                   [kBnMaxBlocks][2][128] | scale[C] | shift[C] | sum1[C] | sum2[C]
+constexpr int kBnGroup = 128;        // channels per channel group
+constexpr int kBnMaxBlocks = 1024;   // x * Y
+constexpr int kBnMaxGroups = 64;     // C <= 8192
+
 struct BnWs {
-  double* s1;
-  double* s2;
+  float* part;
   float* scale;
   float* shift;
+  float* sum1;
+  float* sum2;
+  unsigned* counters;
 };
 BnWs bn_ws(void* ws, int C) {
+  // counters first: their address must not depend on the call's C (the
+  // workspace is shared by layers of different widths)
   BnWs w;
-  w.s1 = static_cast<double*>(ws);
-  w.s2 = w.s1 + C;
-  w.scale = reinterpret_cast<float*>(w.s2 + C);
+  w.counters = static_cast<unsigned*>(ws);
+  w.part = reinterpret_cast<float*>(w.counters + kBnMaxGroups);
+  w.scale = w.part + static_cast<size_t>(kBnMaxBlocks) * 2 * kBnGroup;
   w.shift = w.scale + C;
+  w.sum1 = w.shift + C;
+  w.sum2 = w.sum1 + C;
   return w;
 }
 
-// Block tile: kLanes float4 channel groups x (256 / kLanes) row lanes.
-// gridDim.x covers channel groups, gridDim.y splits the rows.
-// mode 0: s1 += x, s2 += x^2
-// mode 1: g = dy * relu_mask(x) ; s1 += g, s2 += g * xhat
+struct BnArgs {
+  const float* x;
+  const float* dy;
+  long long M;
+  int C, lanes, Y, relu;
+  const float* gamma;
+  const float* beta;
+  const float* mean;     // mode 1
+  const float* invstd;   // mode 1
+  float eps, momentum;
+  float* save_mean;      // mode 0 outputs
+  float* save_invstd;
+  float* run_mean;
+  float* run_var;
+  float* dgamma;         // mode 1 outputs
+  float* dbeta;
+  BnWs w;
+};
+
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) bn_reduce_kernel(
-    const float* __restrict__ x, const float* __restrict__ dy, long long M, int C,
-    int lanes, const float* __restrict__ mean, const float* __restrict__ invstd,
-    const float* __restrict__ gamma, const float* __restrict__ beta, int relu,
-    double* __restrict__ s1, double* __restrict__ s2) {
+__global__ void __launch_bounds__(kThreads) bn_reduce_kernel(const BnArgs a) {
   __shared__ float red[2][kThreads][4];
+  __shared__ int is_last;
+  const int lanes = a.lanes;
   const int lane_c = threadIdx.x % lanes;
   const int lane_r = threadIdx.x / lanes;
   const int rows_per_pass = kThreads / lanes;
   const int c = (blockIdx.x * lanes + lane_c) * 4;
-  const bool c_ok = c < C;
-  const long long rows_per_block = (M + gridDim.y - 1) / gridDim.y;
+  const bool c_ok = c < a.C;
+  const long long rows_per_block = (a.M + a.Y - 1) / a.Y;
   const long long r_begin = blockIdx.y * rows_per_block;
-  const long long r_end = min(M, r_begin + rows_per_block);
+  const long long r_end = min(a.M, r_begin + rows_per_block);
 
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
-  float mu[4], is[4], ga[4], be[4];
+  float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0},
+        be[4] = {0, 0, 0, 0};
   if (MODE == 1 && c_ok) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      mu[j] = mean[c + j];
-      is[j] = invstd[c + j];
-      ga[j] = gamma[c + j];
-      be[j] = beta[c + j];
+      mu[j] = a.mean[c + j];
+      is[j] = a.invstd[c + j];
+      ga[j] = a.gamma[c + j];
+      be[j] = a.beta[c + j];
     }
   }
-  if (c_ok) {
-    for (long long r = r_begin + lane_r; r < r_end; r += rows_per_pass) {
-      const float4 v = *reinterpret_cast<const float4*>(x + r * C + c);
-      const float xv[4] = {v.x, v.y, v.z, v.w};
-      if (MODE == 0) {
+  auto consume = [&](const float4 v, const float4 d) {
+    const float xv[4] = {v.x, v.y, v.z, v.w};
+    if (MODE == 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          a0[j] += xv[j];
-          a1[j] += xv[j] * xv[j];
-        }
-      } else {
-        const float4 d = *reinterpret_cast<const float4*>(dy + r * C + c);
-        const float dv[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float xh = (xv[j] - mu[j]) * is[j];
-          float g = dv[j];
-          if (relu && (xh * ga[j] + be[j]) <= 0.f) g = 0.f;
-          a0[j] += g;
-          a1[j] += g * xh;
-        }
+      for (int j = 0; j < 4; ++j) {
+        a0[j] += xv[j];
+        a1[j] += xv[j] * xv[j];
       }
+    } else {
+      const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float xh = (xv[j] - mu[j]) * is[j];
+        float g = dv[j];
+        if (a.relu && (xh * ga[j] + be[j]) <= 0.f) g = 0.f;
+        a0[j] += g;
+        a1[j] += g * xh;
+      }
+    }
+  };
+  if (c_ok) {
+    long long r = r_begin + lane_r;
+    const long long step = rows_per_pass;
+    for (; r + 3 * step < r_end; r += 4 * step) {  // 4 rows in flight
+      float4 v[4], d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * a.C + c));
+        if (MODE == 1) d[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * a.C + c));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) consume(v[u], MODE == 1 ? d[u] : v[u]);
+    }
+    for (; r < r_end; r += step) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * a.C + c));
+      const float4 d = MODE == 1 ? __ldg(reinterpret_cast<const float4*>(a.dy + r * a.C + c)) : v;
+      consume(v, d);
     }
   }
 #pragma unroll
@@ -108,8 +155,10 @@ __global__ void __launch_bounds__(kThreads) bn_reduce_kernel(
     red[1][threadIdx.x][j] = a1[j];
   }
   __syncthreads();
-  if (lane_r == 0 && c_ok) {
-    double t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
+  // block partial for this block's channels (row lanes summed in order)
+  const size_t slot = static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x) * 2 * kBnGroup;
+  if (lane_r == 0) {
+    float t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
     for (int rr = 0; rr < rows_per_pass; ++rr) {
       const int src = rr * lanes + lane_c;
 #pragma unroll
@@ -118,35 +167,54 @@ __global__ void __launch_bounds__(kThreads) bn_reduce_kernel(
         t1[j] += red[1][src][j];
       }
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      atomicAdd(&s1[c + j], t0[j]);
-      atomicAdd(&s2[c + j], t1[j]);
+    *reinterpret_cast<float4*>(a.w.part + slot + lane_c * 4) = make_float4(t0[0], t0[1], t0[2], t0[3]);
+    *reinterpret_cast<float4*>(a.w.part + slot + kBnGroup + lane_c * 4) =
+        make_float4(t1[0], t1[1], t1[2], t1[3]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(&a.w.counters[blockIdx.x], 1u);
+    is_last = (t == gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // finalise the channels of this group: thread t -> channel t (< 128), sums
+  // in slot order
+  const int ch_in_group = lanes * 4;
+  for (int t = threadIdx.x; t < ch_in_group; t += kThreads) {
+    const int ch = blockIdx.x * ch_in_group + t;
+    if (ch >= a.C) continue;
+    double s1 = 0.0, s2 = 0.0;
+    for (int y = 0; y < static_cast<int>(gridDim.y); ++y) {
+      const float* p = a.w.part + static_cast<size_t>(y * gridDim.x + blockIdx.x) * 2 * kBnGroup;
+      s1 += static_cast<double>(__ldcg(p + t));
+      s2 += static_cast<double>(__ldcg(p + kBnGroup + t));
+    }
+    if (MODE == 0) {
+      const double mean = s1 / static_cast<double>(a.M);
+      double var = s2 / static_cast<double>(a.M) - mean * mean;
+      if (var < 0) var = 0;
+      const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(a.eps)));
+      const float sc = a.gamma[ch] * inv;
+      a.w.scale[ch] = sc;
+      a.w.shift[ch] = a.beta[ch] - static_cast<float>(mean) * sc;
+      if (a.save_mean) a.save_mean[ch] = static_cast<float>(mean);
+      if (a.save_invstd) a.save_invstd[ch] = inv;
+      if (a.run_mean && a.run_var && a.M > 1) {
+        const double unbiased = var * static_cast<double>(a.M) / static_cast<double>(a.M - 1);
+        a.run_mean[ch] = (1.f - a.momentum) * a.run_mean[ch] + a.momentum * static_cast<float>(mean);
+        a.run_var[ch] = (1.f - a.momentum) * a.run_var[ch] + a.momentum * static_cast<float>(unbiased);
+      }
+    } else {
+      a.w.sum1[ch] = static_cast<float>(s1);
+      a.w.sum2[ch] = static_cast<float>(s2);
+      if (a.dbeta) a.dbeta[ch] = static_cast<float>(s1);
+      if (a.dgamma) a.dgamma[ch] = static_cast<float>(s2);
     }
   }
-}
-
-__global__ void bn_fwd_finalize_kernel(int C, long long M, const float* gamma,
-                                       const float* beta, float eps, double* s1, double* s2,
-                                       float* scale, float* shift, float* save_mean,
-                                       float* save_invstd, float* run_mean, float* run_var,
-                                       float momentum) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const double mean = s1[c] / static_cast<double>(M);
-  double var = s2[c] / static_cast<double>(M) - mean * mean;
-  if (var < 0) var = 0;
-  const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
-  const float sc = gamma[c] * inv;
-  scale[c] = sc;
-  shift[c] = beta[c] - static_cast<float>(mean) * sc;
-  if (save_mean) save_mean[c] = static_cast<float>(mean);
-  if (save_invstd) save_invstd[c] = inv;
-  if (run_mean && run_var && M > 1) {
-    const double unbiased = var * static_cast<double>(M) / static_cast<double>(M - 1);
-    run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * static_cast<float>(mean);
-    run_var[c] = (1.f - momentum) * run_var[c] + momentum * static_cast<float>(unbiased);
-  }
+  if (threadIdx.x == 0) a.w.counters[blockIdx.x] = 0u;  // re-arm for the next launch
 }
 
 __global__ void __launch_bounds__(kThreads) bn_apply_kernel(
@@ -172,20 +240,12 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(
   }
 }
 
-__global__ void bn_bwd_finalize_kernel(int C, const double* s1, const double* s2,
-                                       float* dgamma, float* dbeta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  dbeta[c] = static_cast<float>(s1[c]);
-  dgamma[c] = static_cast<float>(s2[c]);
-}
-
 // dx = gamma*invstd * (g - mean(g) - xhat * mean(g*xhat))
 __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(
     const float* __restrict__ x, const float* __restrict__ dy, long long total4, int C4,
     long long M, const float* __restrict__ gamma, const float* __restrict__ beta,
     const float* __restrict__ mean, const float* __restrict__ invstd,
-    const double* __restrict__ s1, const double* __restrict__ s2, int relu,
+    const float* __restrict__ s1, const float* __restrict__ s2, int relu,
     float* __restrict__ dx, int dx_beta) {
   const float invM = 1.f / static_cast<float>(M);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total4;
@@ -202,8 +262,8 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(
       const float xh = (xv[j] - mean[c + j]) * is;
       float g = dv[j];
       if (relu && (xh * ga + beta[c + j]) <= 0.f) g = 0.f;
-      const float mg = static_cast<float>(s1[c + j]) * invM;
-      const float mgx = static_cast<float>(s2[c + j]) * invM;
+      const float mg = s1[c + j] * invM;
+      const float mgx = s2[c + j] * invM;
       o[j] = ga * is * (g - mg - xh * mgx);
     }
     float4 r = make_float4(o[0], o[1], o[2], o[3]);
@@ -218,18 +278,20 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(
   }
 }
 
+// grid of the reduction: channel groups of lanes*4 <= 128 channels, Y row
+// splits so that x*Y ~ 4 blocks per SM (<= kBnMaxBlocks), >= 32 rows each
 void bn_reduce_launch_dims(long long M, int C, int* lanes, dim3* grid) {
   int l = C / 4;
-  if (l > 32) l = 32;
+  if (l > kBnGroup / 4) l = kBnGroup / 4;
   if (l < 1) l = 1;
   *lanes = l;
   const int cgroups = (C / 4 + l - 1) / l;
-  // enough row splits for ~8 blocks per SM overall, each >= 64 rows
-  long long ysplit = (148LL * 8 + cgroups - 1) / cgroups;
-  const long long max_split = (M + 63) / 64;
-  if (ysplit > max_split) ysplit = max_split;
-  if (ysplit < 1) ysplit = 1;
-  *grid = dim3(cgroups, static_cast<unsigned>(ysplit));
+  long long y = (148LL * 4 + cgroups - 1) / cgroups;
+  const long long max_y = (M + 31) / 32;
+  if (y > max_y) y = max_y;
+  if (y > kBnMaxBlocks / cgroups) y = kBnMaxBlocks / cgroups;
+  if (y < 1) y = 1;
+  *grid = dim3(cgroups, static_cast<unsigned>(y));
 }
 
 // ---------------------------------------------------------------------------
@@ -327,48 +389,61 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int n, int h, in
 }
 
 // gradient routed to the first maximum of each window (row-major scan),
-// recomputed from the input; one thread per input element
+// recomputed from the input; one thread per 4 channels of an input pixel
+// (float4 gathers over the <= ceil(k/stride)^2 windows covering it)
 __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy,
-                                   int n, int h, int w, int c, int kr, int ks, int stride,
+                                   int n, int h, int w, int c4, int kr, int ks, int stride,
                                    int pad, int p, int q, float* __restrict__ dx) {
-  const long long total = static_cast<long long>(n) * h * w * c;
+  const long long total = static_cast<long long>(n) * h * w * c4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* dy4 = reinterpret_cast<const float4*>(dy);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int cc = static_cast<int>(i % c);
-    long long t = i / c;
+    const int cg = static_cast<int>(i % c4);
+    long long t = i / c4;
     const int ww = static_cast<int>(t % w);
     t /= w;
     const int hh = static_cast<int>(t % h);
     const int nn = static_cast<int>(t / h);
-    float acc = 0.f;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
     const int p_lo = max(0, (hh + pad - kr + stride) / stride);
     const int p_hi = min(p - 1, (hh + pad) / stride);
     const int q_lo = max(0, (ww + pad - ks + stride) / stride);
     const int q_hi = min(q - 1, (ww + pad) / stride);
+    const long long img = static_cast<long long>(nn) * h;
     for (int pp = p_lo; pp <= p_hi; ++pp) {
       for (int qq = q_lo; qq <= q_hi; ++qq) {
-        // recompute the window argmax
-        float best = -INFINITY;
-        int bh = -1, bw = -1;
+        // window argmax per channel (first maximum in row-major order)
+        float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int bpos[4] = {-1, -1, -1, -1};
         for (int r = 0; r < kr; ++r) {
           const int ih = pp * stride - pad + r;
           if (ih < 0 || ih >= h) continue;
           for (int s = 0; s < ks; ++s) {
             const int iw = qq * stride - pad + s;
             if (iw < 0 || iw >= w) continue;
-            const float v = x[((static_cast<long long>(nn) * h + ih) * w + iw) * c + cc];
-            if (v > best) {
-              best = v;
-              bh = ih;
-              bw = iw;
-            }
+            const float4 v = __ldg(x4 + ((img + ih) * w + iw) * c4 + cg);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            const int pos = ih * w + iw;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (vv[j] > best[j]) {
+                best[j] = vv[j];
+                bpos[j] = pos;
+              }
           }
         }
-        if (bh == hh && bw == ww)
-          acc += dy[((static_cast<long long>(nn) * p + pp) * q + qq) * c + cc];
+        const int me = hh * w + ww;
+        if (bpos[0] == me || bpos[1] == me || bpos[2] == me || bpos[3] == me) {
+          const float4 g = __ldg(dy4 + ((static_cast<long long>(nn) * p + pp) * q + qq) * c4 + cg);
+          const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (bpos[j] == me) acc[j] += gv[j];
+        }
       }
     }
-    dx[i] = acc;
+    reinterpret_cast<float4*>(dx)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
 }
 
@@ -415,32 +490,47 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// one warp per row
-__global__ void xent_kernel(const float* __restrict__ logits, const int* __restrict__ labels,
-                            int rows, int classes, float* loss, float* dlogits,
-                            float* dbias) {
-  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+// Softmax cross-entropy in one block (the batch is k* rows): one warp per
+// row, then the mean loss and the bias gradient (column sums of dlogits)
+// are summed in row order -- deterministic, no atomics.
+constexpr int kXentThreads = 1024;
+__global__ void __launch_bounds__(kXentThreads) xent_kernel(
+    const float* __restrict__ logits, const int* __restrict__ labels, int rows, int classes,
+    float* loss, float* dlogits, float* dbias) {
+  __shared__ float row_loss[kXentThreads / 32];
+  const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const float* z = logits + static_cast<long long>(row) * classes;
-  float mx = -INFINITY;
-  for (int j = lane; j < classes; j += 32) mx = fmaxf(mx, z[j]);
-  mx = warp_max(mx);
-  float se = 0.f;
-  for (int j = lane; j < classes; j += 32) se += expf(z[j] - mx);
-  se = warp_sum(se);
-  const int y = labels[row];
-  if (loss && lane == 0) {
-    const float lse = mx + logf(se);
-    atomicAdd(loss, (lse - z[y]) / static_cast<float>(rows));
+  const int nw = kXentThreads / 32;
+  float my_loss = 0.f;  // lane 0 of each warp: sum over its rows, in order
+  for (int row = warp; row < rows; row += nw) {
+    const float* z = logits + static_cast<long long>(row) * classes;
+    float mx = -INFINITY;
+    for (int j = lane; j < classes; j += 32) mx = fmaxf(mx, z[j]);
+    mx = warp_max(mx);
+    float se = 0.f;
+    for (int j = lane; j < classes; j += 32) se += expf(z[j] - mx);
+    se = warp_sum(se);
+    const int y = labels[row];
+    if (lane == 0) my_loss += mx + logf(se) - z[y];
+    if (dlogits) {
+      const float inv = 1.f / se;
+      float* d = dlogits + static_cast<long long>(row) * classes;
+      for (int j = lane; j < classes; j += 32)
+        d[j] = (expf(z[j] - mx) * inv - (j == y ? 1.f : 0.f)) / static_cast<float>(rows);
+    }
   }
-  if (dlogits) {
-    const float inv = 1.f / se;
-    float* d = dlogits + static_cast<long long>(row) * classes;
-    for (int j = lane; j < classes; j += 32) {
-      const float g = (expf(z[j] - mx) * inv - (j == y ? 1.f : 0.f)) / static_cast<float>(rows);
-      d[j] = g;
-      if (dbias) atomicAdd(&dbias[j], g);
+  if (lane == 0) row_loss[warp] = my_loss;
+  __syncthreads();
+  if (loss && threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < nw; ++w) t += row_loss[w];
+    *loss = t / static_cast<float>(rows);
+  }
+  if (dbias && dlogits) {
+    for (int j = threadIdx.x; j < classes; j += kXentThreads) {
+      float t = 0.f;
+      for (int row = 0; row < rows; ++row) t += dlogits[static_cast<long long>(row) * classes + j];
+      dbias[j] = t;
     }
   }
 }
@@ -496,25 +586,34 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, int n, int c, i
 using namespace accudnn;
 
 extern "C" unsigned long long accudnn_bn_workspace_bytes(int C) {
-  return static_cast<unsigned long long>(C) * (2 * sizeof(double) + 2 * sizeof(float));
+  return sizeof(float) * (static_cast<unsigned long long>(kBnMaxBlocks) * 2 * kBnGroup + 4ull * C) +
+         sizeof(unsigned) * kBnMaxGroups;
 }
 
 extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* gamma,
                               const float* beta, float eps, int relu, float* y,
                               float* save_mean, float* save_invstd, float* running_mean,
                               float* running_var, float momentum, void* ws, void* stream) {
-  if ((C & 3) || M <= 0) return static_cast<int>(cudaErrorInvalidValue);
+  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   const BnWs w = bn_ws(ws, C);
   cudaStream_t st = S(stream);
-  cudaMemsetAsync(w.s1, 0, 2 * sizeof(double) * C, st);
-  int lanes;
+  BnArgs a{};
+  a.x = x;
+  a.M = M;
+  a.C = C;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.eps = eps;
+  a.momentum = momentum;
+  a.save_mean = save_mean;
+  a.save_invstd = save_invstd;
+  a.run_mean = running_mean;
+  a.run_var = running_var;
+  a.w = w;
   dim3 grid;
-  bn_reduce_launch_dims(M, C, &lanes, &grid);
-  bn_reduce_kernel<0><<<grid, kThreads, 0, st>>>(x, nullptr, M, C, lanes, nullptr, nullptr,
-                                                 nullptr, nullptr, 0, w.s1, w.s2);
-  bn_fwd_finalize_kernel<<<(C + 255) / 256, 256, 0, st>>>(
-      C, M, gamma, beta, eps, w.s1, w.s2, w.scale, w.shift, save_mean, save_invstd,
-      running_mean, running_var, momentum);
+  bn_reduce_launch_dims(M, C, &a.lanes, &grid);
+  a.Y = static_cast<int>(grid.y);
+  bn_reduce_kernel<0><<<grid, kThreads, 0, st>>>(a);
   const long long total4 = M * C / 4;
   bn_apply_kernel<<<grid_for(total4, kThreads), kThreads, 0, st>>>(x, total4, C / 4, w.scale,
                                                                    w.shift, relu, y);
@@ -525,20 +624,29 @@ extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int 
                               const float* gamma, const float* beta, const float* save_mean,
                               const float* save_invstd, int relu, float* dx, int dx_beta,
                               float* dgamma, float* dbeta, void* ws, void* stream) {
-  if ((C & 3) || M <= 0) return static_cast<int>(cudaErrorInvalidValue);
+  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   const BnWs w = bn_ws(ws, C);
   cudaStream_t st = S(stream);
-  cudaMemsetAsync(w.s1, 0, 2 * sizeof(double) * C, st);
-  int lanes;
+  BnArgs a{};
+  a.x = x;
+  a.dy = dy;
+  a.M = M;
+  a.C = C;
+  a.relu = relu;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.mean = save_mean;
+  a.invstd = save_invstd;
+  a.dgamma = dgamma;
+  a.dbeta = dbeta;
+  a.w = w;
   dim3 grid;
-  bn_reduce_launch_dims(M, C, &lanes, &grid);
-  bn_reduce_kernel<1><<<grid, kThreads, 0, st>>>(x, dy, M, C, lanes, save_mean, save_invstd,
-                                                 gamma, beta, relu, w.s1, w.s2);
-  if (dgamma && dbeta)
-    bn_bwd_finalize_kernel<<<(C + 255) / 256, 256, 0, st>>>(C, w.s1, w.s2, dgamma, dbeta);
+  bn_reduce_launch_dims(M, C, &a.lanes, &grid);
+  a.Y = static_cast<int>(grid.y);
+  bn_reduce_kernel<1><<<grid, kThreads, 0, st>>>(a);
   const long long total4 = M * C / 4;
   bn_bwd_dx_kernel<<<grid_for(total4, kThreads), kThreads, 0, st>>>(
-      x, dy, total4, C / 4, M, gamma, beta, save_mean, save_invstd, w.s1, w.s2, relu, dx,
+      x, dy, total4, C / 4, M, gamma, beta, save_mean, save_invstd, w.sum1, w.sum2, relu, dx,
       dx_beta);
   return static_cast<int>(cudaGetLastError());
 }
@@ -587,9 +695,10 @@ extern "C" int accudnn_maxpool_fwd(const float* x, int n, int h, int w, int c, i
 extern "C" int accudnn_maxpool_bwd(const float* x, const float* dy, int n, int h, int w, int c,
                                    int kr, int ks, int stride, int pad, int p, int q, float* dx,
                                    void* stream) {
-  const long long total = static_cast<long long>(n) * h * w * c;
+  if (c & 3) return static_cast<int>(cudaErrorInvalidValue);
+  const long long total = static_cast<long long>(n) * h * w * (c / 4);
   maxpool_bwd_kernel<<<grid_for(total, kThreads), kThreads, 0, S(stream)>>>(
-      x, dy, n, h, w, c, kr, ks, stride, pad, p, q, dx);
+      x, dy, n, h, w, c / 4, kr, ks, stride, pad, p, q, dx);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -614,17 +723,15 @@ extern "C" int accudnn_bias_add(float* y, const float* bias, long long m, int n,
 
 extern "C" int accudnn_xent_fwd(const float* logits, const int* labels, int rows, int classes,
                                 float* loss, void* stream) {
-  cudaMemsetAsync(loss, 0, sizeof(float), S(stream));
-  xent_kernel<<<(rows + 7) / 8, 256, 0, S(stream)>>>(logits, labels, rows, classes, loss,
-                                                    nullptr, nullptr);
+  xent_kernel<<<1, kXentThreads, 0, S(stream)>>>(logits, labels, rows, classes, loss, nullptr,
+                                                 nullptr);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int accudnn_xent_bwd(const float* logits, const int* labels, int rows, int classes,
                                 float* dlogits, float* dbias, void* stream) {
-  if (dbias) cudaMemsetAsync(dbias, 0, sizeof(float) * classes, S(stream));
-  xent_kernel<<<(rows + 7) / 8, 256, 0, S(stream)>>>(logits, labels, rows, classes, nullptr,
-                                                    dlogits, dbias);
+  xent_kernel<<<1, kXentThreads, 0, S(stream)>>>(logits, labels, rows, classes, nullptr,
+                                                 dlogits, dbias);
   return static_cast<int>(cudaGetLastError());
 }
 

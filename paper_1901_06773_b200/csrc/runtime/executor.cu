@@ -160,6 +160,7 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaMemset(I.grads, 0, pbytes), "memset");
   ck(cudaMemset(I.momentum_buf, 0, pbytes), "memset");
   ck(cudaMemset(I.stats, 0, sbytes), "memset");
+  ck(cudaMemset(I.bn_ws, 0, wsbytes), "memset");
   // running variance starts at 1
   {
     std::vector<float> st(static_cast<size_t>(std::max<long long>(4, net_.n_stats)), 0.f);

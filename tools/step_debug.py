@@ -19,6 +19,7 @@ def tf32(t, mode):
 arch, image, classes, k = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
 _, desc = trainer.export_network(arch, image, classes)
 params = trainer.init_params(desc, seed=1)
+if os.environ.get("ACCUDNN_PRECISE"): trainer._lib().accudnn_set_conv_math(1)
 ex = trainer.Executor(arch, image, classes, k=k)
 ex.set_params(params)
 g = np.random.default_rng(0)
