@@ -32,20 +32,28 @@ int grid_for(long long work, int per_block, int cap = 148 * 16) {
 // ---------------------------------------------------------------------------
 // Per-channel reductions are deterministic (no atomics on data): the grid is
 // (channel groups of <= 128 channels) x (Y row splits); every block writes
-// its partial sums to its own slot part[y][2][128-channel group], and the last
-// block of each channel group (arrival counter, re-armed by that block)
-// sums the Y slots in slot order in double precision and finalises:
+// its partial sums to its own slot part[y][2][128-channel group].  Slots are
+// combined in two fixed-shape levels: the last block to arrive in each team
+// of kBnTeam consecutive row splits sums the team's slots in order into a
+// team slot, and the last team of a channel group sums the team slots in
+// order in double precision and finalises (arrival counters are re-armed by
+// the blocks that consumed them):
 //   mode 0 (forward):  mean, invstd, scale = gamma*invstd, shift, running stats
 //   mode 1 (backward): s1 = sum g, s2 = sum g*xhat (g = dy * relu mask) ->
 //                      dbeta, dgamma and the two sums for the dx kernel.
-// Workspace layout: counters (uint) [kBnMaxGroups] | part (float)
-//                   [kBnMaxBlocks][2][128] | scale[C] | shift[C] | sum1[C] | sum2[C]
+// Workspace layout: counters (uint) [kBnMaxGroups * (1 + kBnMaxTeams)] |
+//   part (float) [kBnMaxBlocks][2][128] | tpart [kBnMaxBlocks][2][128] |
+//   scale[C] | shift[C] | sum1[C] | sum2[C]
 constexpr int kBnGroup = 128;        // channels per channel group
 constexpr int kBnMaxBlocks = 1024;   // x * Y
 constexpr int kBnMaxGroups = 64;     // C <= 8192
+constexpr int kBnTeam = 16;          // row splits per first-level team
+constexpr int kBnMaxTeams = kBnMaxBlocks / kBnTeam;
+constexpr int kBnCounters = kBnMaxGroups * (1 + kBnMaxTeams);
 
 struct BnWs {
   float* part;
+  float* tpart;
   float* scale;
   float* shift;
   float* sum1;
@@ -57,8 +65,9 @@ BnWs bn_ws(void* ws, int C) {
   // workspace is shared by layers of different widths)
   BnWs w;
   w.counters = static_cast<unsigned*>(ws);
-  w.part = reinterpret_cast<float*>(w.counters + kBnMaxGroups);
-  w.scale = w.part + static_cast<size_t>(kBnMaxBlocks) * 2 * kBnGroup;
+  w.part = reinterpret_cast<float*>(w.counters + kBnCounters);
+  w.tpart = w.part + static_cast<size_t>(kBnMaxBlocks) * 2 * kBnGroup;
+  w.scale = w.tpart + static_cast<size_t>(kBnMaxBlocks) * 2 * kBnGroup;
   w.shift = w.scale + C;
   w.sum1 = w.shift + C;
   w.sum2 = w.sum1 + C;
@@ -171,24 +180,44 @@ __global__ void __launch_bounds__(kThreads) bn_reduce_kernel(const BnArgs a) {
     *reinterpret_cast<float4*>(a.w.part + slot + kBnGroup + lane_c * 4) =
         make_float4(t1[0], t1[1], t1[2], t1[3]);
   }
+  const int ch_in_group = lanes * 4;
+  const int gx = gridDim.x;
+  // ---- level 1: the last block of this team sums the team's slots ----
+  const int team = blockIdx.y / kBnTeam;
+  const int team_lo = team * kBnTeam;
+  const int team_n = min(kBnTeam, static_cast<int>(gridDim.y) - team_lo);
+  unsigned* tcount = a.w.counters + kBnMaxGroups + blockIdx.x * kBnMaxTeams + team;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(&a.w.counters[blockIdx.x], 1u);
-    is_last = (t == gridDim.y - 1);
-  }
+  if (threadIdx.x == 0) is_last = (atomicAdd(tcount, 1u) == static_cast<unsigned>(team_n - 1));
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // finalise the channels of this group: thread t -> channel t (< 128), sums
-  // in slot order
-  const int ch_in_group = lanes * 4;
+  for (int v = threadIdx.x; v < 2 * kBnGroup; v += kThreads) {
+    if ((v & (kBnGroup - 1)) >= ch_in_group) continue;
+    float t = 0.f;
+#pragma unroll 4
+    for (int y = team_lo; y < team_lo + team_n; ++y)
+      t += __ldcg(a.w.part + static_cast<size_t>(y * gx + blockIdx.x) * 2 * kBnGroup + v);
+    a.w.tpart[static_cast<size_t>(team * gx + blockIdx.x) * 2 * kBnGroup + v] = t;
+  }
+  if (threadIdx.x == 0) *tcount = 0u;  // re-arm
+  // ---- level 2: the last team of the channel group finalises ----
+  const int nteams = (gridDim.y + kBnTeam - 1) / kBnTeam;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    is_last = (atomicAdd(&a.w.counters[blockIdx.x], 1u) == static_cast<unsigned>(nteams - 1));
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
   for (int t = threadIdx.x; t < ch_in_group; t += kThreads) {
     const int ch = blockIdx.x * ch_in_group + t;
     if (ch >= a.C) continue;
     double s1 = 0.0, s2 = 0.0;
-    for (int y = 0; y < static_cast<int>(gridDim.y); ++y) {
-      const float* p = a.w.part + static_cast<size_t>(y * gridDim.x + blockIdx.x) * 2 * kBnGroup;
+#pragma unroll 4
+    for (int tm = 0; tm < nteams; ++tm) {
+      const float* p = a.w.tpart + static_cast<size_t>(tm * gx + blockIdx.x) * 2 * kBnGroup;
       s1 += static_cast<double>(__ldcg(p + t));
       s2 += static_cast<double>(__ldcg(p + kBnGroup + t));
     }
@@ -586,8 +615,8 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, int n, int c, i
 using namespace accudnn;
 
 extern "C" unsigned long long accudnn_bn_workspace_bytes(int C) {
-  return sizeof(float) * (static_cast<unsigned long long>(kBnMaxBlocks) * 2 * kBnGroup + 4ull * C) +
-         sizeof(unsigned) * kBnMaxGroups;
+  return sizeof(float) * (2ull * kBnMaxBlocks * 2 * kBnGroup + 4ull * C) +
+         sizeof(unsigned) * kBnCounters;
 }
 
 extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* gamma,
