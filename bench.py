@@ -257,6 +257,8 @@ def run_ours(args):
     from paper_1901_06773_b200 import planner, trainer
 
     world, rank, local = dist_env()
+    if "ACCUDNN_PDL" in os.environ:  # A/B switch for programmatic dependent launch
+        trainer._lib().accudnn_set_pdl(int(os.environ["ACCUDNN_PDL"]))
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)

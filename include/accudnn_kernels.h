@@ -42,6 +42,14 @@ int accudnn_set_conv_impl(int impl);
  * lazily allocated default of that size (64 MiB initially), bytes == 0
  * disables split-K.  Splits are limited so that splits * M * N * 4 <= bytes. */
 int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes);
+/* programmatic dependent launch for every kernel (default 0): the next
+ * kernel's prologue overlaps the previous one's tail.  Returns the previous. */
+int accudnn_set_pdl(int enable);
+/* 1: tune (tile width, split-K) per convolution shape on its first
+ * overwrite (beta = 0) call outside stream capture -- every candidate is
+ * timed with CUDA events and the fastest is cached for the process; 0: the
+ * analytic choice.  Returns the previous setting. */
+int accudnn_conv_autotune(int enable);
 /* splits <= 0 picks a split-K factor automatically (TMA path: deterministic
  * workspace fix-up; cp.async fallback: fp32 atomics) */
 int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,

@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "accudnn_kernels.h"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 
 namespace accudnn {
@@ -123,6 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem = *tmem_slot;
   const uint32_t smem_base = ptx::smem_u32(smem);
 
@@ -418,7 +421,7 @@ int launch(const Args& a, int splits, cudaStream_t stream) {
     configured = true;
   }
   dim3 grid((a.M + kBM - 1) / kBM, (a.Ng + BN - 1) / BN, splits);
-  conv_igemm_kernel<MODE, BN, PRECISE><<<grid, kThreads, smem, stream>>>(a);
+  launch_pdl(conv_igemm_kernel<MODE, BN, PRECISE>, grid, kThreads, smem, stream, a);
   return static_cast<int>(cudaGetLastError());
 }
 

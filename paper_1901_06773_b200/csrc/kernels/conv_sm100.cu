@@ -35,11 +35,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
+#include <unordered_map>
 #include <cstdio>
 #include <cstring>
 
 #include "accudnn_kernels.h"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 
 namespace accudnn {
@@ -162,6 +165,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t smem_base = ptx::smem_u32(smem);
+  // everything above overlapped the previous kernel's tail (PDL)
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -374,6 +380,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // slices always summed in slice order.  One float4 per thread-iteration,
 // grid-stride over the M x Ng/4 output vectors (coalesced rows).
 __global__ void __launch_bounds__(256) conv_splitk_reduce_kernel(const Prob a) {
+  pdl_wait();
+  pdl_trigger();
   const int ng4 = a.Ng >> 2;
   const long long total = static_cast<long long>(a.M) * ng4;
   const long long slice = static_cast<long long>(a.M) * a.Ng;
@@ -383,12 +391,19 @@ __global__ void __launch_bounds__(256) conv_splitk_reduce_kernel(const Prob a) {
     const int c = static_cast<int>(i - static_cast<long long>(m) * ng4) * 4;
     const float* src = a.ws + static_cast<long long>(m) * a.Ng + c;
     float4 o = __ldcg(reinterpret_cast<const float4*>(src));
-    for (int s = 1; s < a.splits; ++s) {
-      const float4 p = __ldcg(reinterpret_cast<const float4*>(src + s * slice));
-      o.x += p.x;
-      o.y += p.y;
-      o.z += p.z;
-      o.w += p.w;
+    for (int s0 = 1; s0 < a.splits; s0 += 8) {  // 8 slices in flight, summed in order
+      float4 p[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < a.splits) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + u) * slice));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < a.splits) {
+          o.x += p[u].x;
+          o.y += p[u].y;
+          o.z += p[u].z;
+          o.w += p[u].w;
+        }
     }
     float4* d = reinterpret_cast<float4*>(a.out + out_row(a, m) + c);
     if (a.beta) {
@@ -537,27 +552,13 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Prob& a, cudaSt
     configured = true;
   }
   const int grid = static_cast<int>(std::min<long long>(a.units, sm_count()));
-  conv_sm100_kernel<MODE, BN, STAGES><<<grid, kThreads, smem, st>>>(ta, tb, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(conv_sm100_kernel<MODE, BN, STAGES>, grid, kThreads, smem, st, ta, tb, a);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
   const long long vec = static_cast<long long>(a.M) * (a.Ng / 4);
   const int rgrid = static_cast<int>(std::min<long long>((vec + 255) / 256, 8LL * sm_count()));
-  conv_splitk_reduce_kernel<<<rgrid, 256, 0, st>>>(a);
+  launch_pdl(conv_splitk_reduce_kernel, rgrid, 256, 0, st, a);
   return static_cast<int>(cudaGetLastError());
-}
-
-template <int MODE, int BN>
-int run(const CUtensorMap& ta, const CUtensorMap& tb, Prob a, cudaStream_t st) {
-  a.tiles_m = (a.M + kBM - 1) / kBM;
-  a.tiles_n = (a.Ng + BN - 1) / BN;
-  const long long tiles = static_cast<long long>(a.tiles_m) * a.tiles_n;
-  a.splits = choose_splits(tiles, a.kb_total, BN, static_cast<long long>(a.M) * a.Ng, a.beta,
-                           ws_capacity());
-  a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
-  a.units = static_cast<int>(tiles * a.splits);
-  a.ws = g_ws.ws;
-  constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
-  return launch_t<MODE, BN, kStages>(ta, tb, a, st);
 }
 
 Prob base_prob(const accudnn_conv_desc* d) {
@@ -591,40 +592,222 @@ ClassDim class_dim(int a, int stride, int pad, int R, int H, int P) {
   return c;
 }
 
+// ---- one GEMM of a convolution, re-launchable with any (BN, splits) -------------
+struct Call {
+  int mode = FWD;
+  Prob a{};           // geometry, GEMM extents, class fields, output, beta
+  const void* A = nullptr;  // operand base pointers (x / dy / w)
+  const void* B = nullptr;
+  int key[14] = {};   // autotune key
+};
+struct Cfg {
+  int bn = 0, splits = 0;
+};
+struct KeyHash {
+  size_t operator()(const std::array<int, 14>& k) const {
+    size_t h = 1469598103934665603ull;
+    for (int v : k) h = (h ^ static_cast<size_t>(v)) * 1099511628211ull;
+    return h;
+  }
+};
+std::unordered_map<std::array<int, 14>, Cfg, KeyHash> g_tuned;
+int g_autotune = 0;
+
+bool bn_ok(const Call& c, int bn) {
+  switch (c.mode) {
+    case FWD:
+      return bn == 64 || c.a.K > bn / 2;  // no tile wider than twice the channels
+    case DGRAD:
+      return (c.a.C % bn == 0 || bn == 64) && (bn == 64 || c.a.C > bn / 2);
+    default:
+      return c.a.C % bn == 0;
+  }
+}
+
+bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb) {
+  const Prob& a = c.a;
+  if (c.mode == FWD) {
+    bool ok;
+    if (a.a_tiled) {
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.C), static_cast<cuuint64_t>(a.M)};
+      const cuuint64_t str[1] = {static_cast<cuuint64_t>(a.C) * 4};
+      const cuuint32_t box[2] = {32, kBM};
+      ok = tiled_map(ta, c.A, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+      const int lo = -a.pad, up = a.pad - (a.R - 1);
+      ok = im2col_map(ta, c.A, a.N, a.H, a.W, a.C, lo, lo, up, up, a.stride, kBM,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    const int Kg = a.R * a.S * a.C;
+    const cuuint64_t bd[2] = {static_cast<cuuint64_t>(Kg), static_cast<cuuint64_t>(a.K)};
+    const cuuint64_t bs[1] = {static_cast<cuuint64_t>(Kg) * 4};
+    const cuuint32_t bbox[2] = {32, static_cast<cuuint32_t>(bn)};
+    return ok && tiled_map(tb, c.B, 2, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (c.mode == DGRAD) {
+    bool ok;
+    if (a.a_tiled) {
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.K),
+                                  static_cast<cuuint64_t>(a.N) * a.P * a.Q};
+      const cuuint64_t str[1] = {static_cast<cuuint64_t>(a.K) * 4};
+      const cuuint32_t box[2] = {32, kBM};
+      ok = tiled_map(ta, c.A, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+      ok = im2col_map(ta, c.A, a.N, a.P, a.Q, a.K, a.lo_h, a.lo_w, a.Hc - a.P + a.lo_h,
+                      a.Wc - a.Q + a.lo_w, 1, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    const cuuint64_t bd[3] = {static_cast<cuuint64_t>(a.C), static_cast<cuuint64_t>(a.R) * a.S,
+                              static_cast<cuuint64_t>(a.K)};
+    const cuuint64_t bs[2] = {static_cast<cuuint64_t>(a.C) * 4,
+                              static_cast<cuuint64_t>(a.C) * a.R * a.S * 4};
+    const cuuint32_t bbox[3] = {32, 1, 32};
+    return ok && tiled_map(tb, c.B, 3, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
+  const int Kg = a.N * a.P * a.Q;
+  const cuuint64_t ad[2] = {static_cast<cuuint64_t>(a.K), static_cast<cuuint64_t>(Kg)};
+  const cuuint64_t as[1] = {static_cast<cuuint64_t>(a.K) * 4};
+  const cuuint32_t abox[2] = {32, 32};
+  bool ok = tiled_map(ta, c.A, 2, ad, as, abox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const int lo = -a.pad, up = a.pad - (a.R - 1);
+  return ok && im2col_map(tb, c.B, a.N, a.H, a.W, a.C, lo, lo, up, up, a.stride, 32,
+                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+template <int MODE>
+int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const Prob& a, int bn,
+                cudaStream_t st) {
+  if (bn == 256) return launch_t<MODE, 256, 4>(ta, tb, a, st);
+  if (bn == 128) return launch_t<MODE, 128, 6>(ta, tb, a, st);
+  return launch_t<MODE, 64, 8>(ta, tb, a, st);
+}
+
+// -1: could not encode the tensor maps (not launched)
+int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  if (!encode(c, cfg.bn, &ta, &tb)) return -1;
+  Prob a = c.a;
+  a.tiles_m = (a.M + kBM - 1) / kBM;
+  a.tiles_n = (a.Ng + cfg.bn - 1) / cfg.bn;
+  a.splits = cfg.splits;
+  a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
+  a.units = a.tiles_m * a.tiles_n * a.splits;
+  a.ws = g_ws.ws;
+  if (c.mode == FWD) return dispatch_bn<FWD>(ta, tb, a, cfg.bn, st);
+  if (c.mode == DGRAD) return dispatch_bn<DGRAD>(ta, tb, a, cfg.bn, st);
+  return dispatch_bn<WGRAD>(ta, tb, a, cfg.bn, st);
+}
+
+bool splits_ok(const Call& c, int s) {
+  if (s < 1 || s > c.a.kb_total) return false;
+  const int per = (c.a.kb_total + s - 1) / s;
+  if ((c.a.kb_total + per - 1) / per != s) return false;
+  return s == 1 || static_cast<size_t>(s) * c.a.M * c.a.Ng * 4 <= ws_capacity();
+}
+
+Cfg model_cfg(const Call& c) {
+  int bn;
+  if (c.mode == FWD) bn = c.a.K >= 256 ? 256 : (c.a.K > 64 ? 128 : 64);
+  else if (c.mode == DGRAD) bn = c.a.C >= 256 ? 256 : (c.a.C > 64 ? 128 : 64);
+  else bn = (c.a.C % 256 == 0) ? 256 : (c.a.C % 128 == 0) ? 128 : 64;
+  if (!bn_ok(c, bn)) bn = 64;
+  const long long tiles =
+      static_cast<long long>((c.a.M + kBM - 1) / kBM) * ((c.a.Ng + bn - 1) / bn);
+  Cfg cfg;
+  cfg.bn = bn;
+  cfg.splits = choose_splits(tiles, c.a.kb_total, bn, static_cast<long long>(c.a.M) * c.a.Ng,
+                             c.a.beta, ws_capacity());
+  return cfg;
+}
+
+// Empirical choice of (BN, splits) for one GEMM: every candidate is run
+// once and then timed (min of 3, CUDA events on the caller's stream).  Only
+// outputs that are overwritten (beta = 0) are tuned, never during stream
+// capture; the result is cached per shape for the life of the process.
+Cfg tune(const Call& c, cudaStream_t st) {
+  static const int kSplits[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64, 96, 128};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  Cfg best = model_cfg(c);
+  float best_ms = 1e30f;
+  for (int bn : {64, 128, 256}) {
+    if (!bn_ok(c, bn)) continue;
+    for (int s : kSplits) {
+      if (!splits_ok(c, s)) continue;
+      const Cfg cand{bn, s};
+      if (launch_cfg(c, cand, st) != 0) {
+        cudaGetLastError();
+        continue;
+      }
+      float t = 1e30f;
+      for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0, st);
+        launch_cfg(c, cand, st);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        t = std::min(t, ms);
+      }
+      if (t < best_ms) {
+        best_ms = t;
+        best = cand;
+      }
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+
+int run_call(const Call& c, cudaStream_t st) {
+  std::array<int, 14> key;
+  std::copy(std::begin(c.key), std::end(c.key), key.begin());
+  Cfg cfg;
+  auto it = g_tuned.find(key);
+  if (it != g_tuned.end() && splits_ok(c, it->second.splits)) {
+    cfg = it->second;
+  } else {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (g_autotune && !c.a.beta && cap == cudaStreamCaptureStatusNone) {
+      cfg = tune(c, st);
+      g_tuned[key] = cfg;
+    } else {
+      cfg = model_cfg(c);
+    }
+  }
+  return launch_cfg(c, cfg, st);
+}
+
+void fill_key(Call& c, const accudnn_conv_desc* d, int cls) {
+  const int k[14] = {c.mode, d->n, d->h, d->w, d->c, d->k, d->r, d->s, d->stride, d->pad,
+                     d->p, d->q, cls, 0};
+  std::copy(k, k + 14, c.key);
+}
+
 }  // namespace
 
 // 0 = not eligible (caller falls back to the cp.async kernel), else launched
 int conv_tma_fwd(const accudnn_conv_desc* d, const float* x, const float* w, float* y, int beta,
                  cudaStream_t st, int* rc) {
   if (!geometry_ok(d) || (d->c % 32) || (d->k % 4)) return 0;
-  Prob a = base_prob(d);
+  Call c;
+  c.mode = FWD;
+  Prob& a = c.a;
+  a = base_prob(d);
   a.M = a.N * a.P * a.Q;
   a.Ng = a.K;
-  const int Kg = a.R * a.S * a.C;
-  a.kb_total = Kg / kBK;
+  a.kb_total = a.R * a.S * a.C / kBK;
   a.out = y;
   a.beta = beta;
   a.a_tiled = (a.R == 1 && a.stride == 1 && a.pad == 0);
-  const int BN = a.K >= 256 ? 256 : (a.K > 64 ? 128 : 64);
-  CUtensorMap ta, tb;
-  bool ok;
-  if (a.a_tiled) {
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.C), static_cast<cuuint64_t>(a.M)};
-    const cuuint64_t str[1] = {static_cast<cuuint64_t>(a.C) * 4};
-    const cuuint32_t box[2] = {32, kBM};
-    ok = tiled_map(&ta, x, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
-  } else {
-    const int lo = -a.pad, up = a.pad - (a.R - 1);
-    ok = im2col_map(&ta, x, a.N, a.H, a.W, a.C, lo, lo, up, up, a.stride, kBM,
-                    CU_TENSOR_MAP_SWIZZLE_128B);
-  }
-  const cuuint64_t bd[2] = {static_cast<cuuint64_t>(Kg), static_cast<cuuint64_t>(a.K)};
-  const cuuint64_t bs[1] = {static_cast<cuuint64_t>(Kg) * 4};
-  const cuuint32_t bbox[2] = {32, static_cast<cuuint32_t>(BN)};
-  ok = ok && tiled_map(&tb, w, 2, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!ok) return 0;
-  *rc = BN == 256 ? run<FWD, 256>(ta, tb, a, st)
-                  : (BN == 128 ? run<FWD, 128>(ta, tb, a, st) : run<FWD, 64>(ta, tb, a, st));
+  c.A = x;
+  c.B = w;
+  fill_key(c, d, 0);
+  const int r = run_call(c, st);
+  if (r == -1) return 0;
+  *rc = r;
   return 1;
 }
 
@@ -644,9 +827,8 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
     if (rows[c].lower < -64 || cols[c].lower < -64 || rows[c].lower > 64 || cols[c].lower > 64)
       return 0;
   }
-  const int BN = d->c >= 256 ? 256 : (d->c > 64 ? 128 : 64);
-  if (d->c % BN && BN != 64) return 0;
   *rc = 0;
+  bool launched = false;
   if (any_empty && !beta) {
     const cudaError_t e = cudaMemsetAsync(
         dx, 0, sizeof(float) * static_cast<size_t>(d->n) * d->h * d->w * d->c, st);
@@ -654,6 +836,7 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
       *rc = static_cast<int>(e);
       return 1;
     }
+    launched = true;
     beta = 1;
   }
   for (int ca = 0; ca < s; ++ca) {
@@ -661,7 +844,10 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
       const ClassDim& cr = rows[ca];
       const ClassDim& cc = cols[cb];
       if (cr.taps == 0 || cc.taps == 0) continue;
-      Prob a = base_prob(d);
+      Call c;
+      c.mode = DGRAD;
+      Prob& a = c.a;
+      a = base_prob(d);
       a.cls_a = ca;
       a.cls_b = cb;
       a.Hc = cr.out;
@@ -680,29 +866,15 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
       a.beta = beta;
       a.a_tiled = (a.Rc == 1 && a.Sc == 1 && a.lo_h == 0 && a.lo_w == 0 && a.Hc == a.P &&
                    a.Wc == a.Q);
-      CUtensorMap ta, tb;
-      bool ok;
-      if (a.a_tiled) {
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.K),
-                                    static_cast<cuuint64_t>(a.N) * a.P * a.Q};
-        const cuuint64_t str[1] = {static_cast<cuuint64_t>(a.K) * 4};
-        const cuuint32_t box[2] = {32, kBM};
-        ok = tiled_map(&ta, dy, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
-      } else {
-        ok = im2col_map(&ta, dy, a.N, a.P, a.Q, a.K, a.lo_h, a.lo_w, a.Hc - a.P + a.lo_h,
-                        a.Wc - a.Q + a.lo_w, 1, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
-      }
-      const cuuint64_t bd[3] = {static_cast<cuuint64_t>(a.C), static_cast<cuuint64_t>(a.R) * a.S,
-                                static_cast<cuuint64_t>(a.K)};
-      const cuuint64_t bs[2] = {static_cast<cuuint64_t>(a.C) * 4,
-                                static_cast<cuuint64_t>(a.C) * a.R * a.S * 4};
-      const cuuint32_t bbox[3] = {32, 1, 32};
-      ok = ok && tiled_map(&tb, w, 3, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-      if (!ok) return *rc ? 1 : 0;  // nothing launched yet on the first class
-      *rc = BN == 256 ? run<DGRAD, 256>(ta, tb, a, st)
-                      : (BN == 128 ? run<DGRAD, 128>(ta, tb, a, st)
-                                   : run<DGRAD, 64>(ta, tb, a, st));
-      if (*rc) return 1;
+      c.A = dy;
+      c.B = w;
+      fill_key(c, d, 1 + ca * s + cb);
+      c.key[13] = beta;
+      const int r = run_call(c, st);
+      if (r == -1) return launched ? (*rc = static_cast<int>(cudaErrorInvalidValue), 1) : 0;
+      launched = true;
+      *rc = r;
+      if (r) return 1;
     }
   }
   return 1;
@@ -710,29 +882,24 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
 
 int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, float* dw,
                    int beta, cudaStream_t st, int* rc) {
-  if (!geometry_ok(d) || (d->c % 32) || (d->k % 4)) return 0;
-  Prob a = base_prob(d);
+  if (!geometry_ok(d) || (d->c % 32) || (d->k % 4) || (d->c % 64)) return 0;
+  Call c;
+  c.mode = WGRAD;
+  Prob& a = c.a;
+  a = base_prob(d);
   a.M = a.K;
   a.Ng = a.R * a.S * a.C;
-  const int Kg = a.N * a.P * a.Q;
   // a ragged last K-block reads past the last output pixel: the im2col walk
   // and the dy tile land out of bounds there and are zero-filled by the TMA
-  a.kb_total = (Kg + kBK - 1) / kBK;
+  a.kb_total = (a.N * a.P * a.Q + kBK - 1) / kBK;
   a.out = dw;
   a.beta = beta;
-  const int BN = (a.C % 256 == 0) ? 256 : (a.C % 128 == 0) ? 128 : (a.C % 64 == 0 ? 64 : 0);
-  if (!BN) return 0;
-  CUtensorMap ta, tb;
-  const cuuint64_t ad[2] = {static_cast<cuuint64_t>(a.K), static_cast<cuuint64_t>(Kg)};
-  const cuuint64_t as[1] = {static_cast<cuuint64_t>(a.K) * 4};
-  const cuuint32_t abox[2] = {32, 32};
-  bool ok = tiled_map(&ta, dy, 2, ad, as, abox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  const int lo = -a.pad, up = a.pad - (a.R - 1);
-  ok = ok && im2col_map(&tb, x, a.N, a.H, a.W, a.C, lo, lo, up, up, a.stride, 32,
-                        CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  if (!ok) return 0;
-  *rc = BN == 256 ? run<WGRAD, 256>(ta, tb, a, st)
-                  : (BN == 128 ? run<WGRAD, 128>(ta, tb, a, st) : run<WGRAD, 64>(ta, tb, a, st));
+  c.A = dy;
+  c.B = x;
+  fill_key(c, d, 0);
+  const int r = run_call(c, st);
+  if (r == -1) return 0;
+  *rc = r;
   return 1;
 }
 
@@ -752,7 +919,7 @@ int conv_splitk_reduce(float* ws, int splits, int M, int Ng, float* out, int bet
   a.beta = beta;
   const long long vec = static_cast<long long>(M) * (Ng / 4);
   const int rgrid = static_cast<int>(std::min<long long>((vec + 255) / 256, 8LL * sm_count()));
-  conv_splitk_reduce_kernel<<<rgrid, 256, 0, st>>>(a);
+  launch_pdl(conv_splitk_reduce_kernel, rgrid, 256, 0, st, a);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -770,4 +937,12 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
   g_ws.owned = false;
   if (!ptr) g_ws_default = static_cast<size_t>(bytes);
   return 0;
+}
+
+// 1: tune (BN, split-K) per convolution shape on first use (beta = 0 calls,
+// outside stream capture), 0: analytic choice.  Returns the previous mode.
+extern "C" int accudnn_conv_autotune(int enable) {
+  const int prev = accudnn::g_autotune;
+  accudnn::g_autotune = enable ? 1 : 0;
+  return prev;
 }

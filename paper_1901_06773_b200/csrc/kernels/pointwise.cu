@@ -9,11 +9,15 @@
 // in E[x^2] - E[x]^2).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "accudnn_kernels.h"
+#include "pdl.cuh"
 
 namespace accudnn {
+int g_pdl = 0;  // measured: PDL slowed the captured step (19.6 vs 18.9 ms), off by default
+float* conv_splitk_workspace(size_t bytes);  // conv_sm100.cu
 namespace {
 
 constexpr int kThreads = 256;
@@ -30,47 +34,34 @@ int grid_for(long long work, int per_block, int cap = 148 * 16) {
 // ---------------------------------------------------------------------------
 // batch normalisation
 // ---------------------------------------------------------------------------
-// Per-channel reductions are deterministic (no atomics on data): the grid is
-// (channel groups of <= 128 channels) x (Y row splits); every block writes
-// its partial sums to its own slot part[y][2][128-channel group].  Slots are
-// combined in two fixed-shape levels: the last block to arrive in each team
-// of kBnTeam consecutive row splits sums the team's slots in order into a
-// team slot, and the last team of a channel group sums the team slots in
-// order in double precision and finalises (arrival counters are re-armed by
-// the blocks that consumed them):
-//   mode 0 (forward):  mean, invstd, scale = gamma*invstd, shift, running stats
-//   mode 1 (backward): s1 = sum g, s2 = sum g*xhat (g = dy * relu mask) ->
-//                      dbeta, dgamma and the two sums for the dx kernel.
-// Workspace layout: counters (uint) [kBnMaxGroups * (1 + kBnMaxTeams)] |
-//   part (float) [kBnMaxBlocks][2][128] | tpart [kBnMaxBlocks][2][128] |
-//   scale[C] | shift[C] | sum1[C] | sum2[C]
+// One cooperative kernel per BN pass (forward: statistics + normalise;
+// backward: (sum g, sum g*xhat) + data gradient), deterministic, no atomics
+// on data:
+//   phase 1  block (channel group bx, row split by) accumulates its rows into
+//            a private slot part[by*gx+bx][2][128]
+//   barrier  grid-wide (all blocks are co-resident: cooperative launch)
+//   phase 2  every block sums the Y slots of its channel group in a fixed
+//            order (chunked over threads, chunks combined in order, fp64) --
+//            all blocks of a group compute bit-identical constants; block
+//            by == 0 writes the per-channel outputs
+//   phase 3  the block normalises / back-propagates the same rows it reduced
+//            (mostly L1/L2 hits)
+// Workspace: barrier words (uint) [kBnCounters] | part (float) [kBnMaxBlocks][2][128]
+constexpr int kBnThreads = 512;
 constexpr int kBnGroup = 128;        // channels per channel group
-constexpr int kBnMaxBlocks = 1024;   // x * Y
+constexpr int kBnMaxBlocks = 1024;   // gx * Y
 constexpr int kBnMaxGroups = 64;     // C <= 8192
-constexpr int kBnTeam = 16;          // row splits per first-level team
-constexpr int kBnMaxTeams = kBnMaxBlocks / kBnTeam;
-constexpr int kBnCounters = kBnMaxGroups * (1 + kBnMaxTeams);
+constexpr int kBnMaxY = 128;         // row splits (bounds phase 2's slot sums)
+constexpr int kBnCounters = 64;
 
 struct BnWs {
+  unsigned* counters;  // [0] arrivals, [1] generation
   float* part;
-  float* tpart;
-  float* scale;
-  float* shift;
-  float* sum1;
-  float* sum2;
-  unsigned* counters;
 };
 BnWs bn_ws(void* ws, int C) {
-  // counters first: their address must not depend on the call's C (the
-  // workspace is shared by layers of different widths)
   BnWs w;
   w.counters = static_cast<unsigned*>(ws);
   w.part = reinterpret_cast<float*>(w.counters + kBnCounters);
-  w.tpart = w.part + static_cast<size_t>(kBnMaxBlocks) * 2 * kBnGroup;
-  w.scale = w.tpart + static_cast<size_t>(kBnMaxBlocks) * 2 * kBnGroup;
-  w.shift = w.scale + C;
-  w.sum1 = w.shift + C;
-  w.sum2 = w.sum1 + C;
   return w;
 }
 
@@ -88,28 +79,54 @@ struct BnArgs {
   float* save_invstd;
   float* run_mean;
   float* run_var;
+  float* y;              // mode 0: normalised output
   float* dgamma;         // mode 1 outputs
   float* dbeta;
+  float* dx;             // mode 1: data gradient (+= when dx_beta)
+  int dx_beta;
   BnWs w;
 };
 
+__device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblocks) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = counters + 1;
+    const unsigned g = *gen;
+    if (atomicAdd(counters, 1u) == nblocks - 1) {
+      counters[0] = 0u;
+      __threadfence();
+      atomicAdd(counters + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) bn_reduce_kernel(const BnArgs a) {
-  __shared__ float red[2][kThreads][4];
-  __shared__ int is_last;
+__global__ void __launch_bounds__(kBnThreads) bn_fused_kernel(const BnArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[2][kBnThreads][4];
+  __shared__ double dsum[kBnThreads];
+  __shared__ float coef[6][kBnGroup];
   const int lanes = a.lanes;
   const int lane_c = threadIdx.x % lanes;
   const int lane_r = threadIdx.x / lanes;
-  const int rows_per_pass = kThreads / lanes;
+  const int rows_per_pass = kBnThreads / lanes;
+  const bool lane_ok = lane_r < rows_per_pass;
   const int c = (blockIdx.x * lanes + lane_c) * 4;
-  const bool c_ok = c < a.C;
+  const bool c_ok = lane_ok && c < a.C;
   const long long rows_per_block = (a.M + a.Y - 1) / a.Y;
   const long long r_begin = blockIdx.y * rows_per_block;
   const long long r_end = min(a.M, r_begin + rows_per_block);
+  const long long C = a.C;
 
+  // ---- phase 1: per-block partial sums ----
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
-  float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0},
-        be[4] = {0, 0, 0, 0};
+  float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0}, be[4] = {0, 0, 0, 0};
   if (MODE == 1 && c_ok) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -139,22 +156,22 @@ __global__ void __launch_bounds__(kThreads) bn_reduce_kernel(const BnArgs a) {
       }
     }
   };
+  const long long step = rows_per_pass;
   if (c_ok) {
     long long r = r_begin + lane_r;
-    const long long step = rows_per_pass;
     for (; r + 3 * step < r_end; r += 4 * step) {  // 4 rows in flight
       float4 v[4], d[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * a.C + c));
-        if (MODE == 1) d[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * a.C + c));
+        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
+        if (MODE == 1) d[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * C + c));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) consume(v[u], MODE == 1 ? d[u] : v[u]);
     }
     for (; r < r_end; r += step) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * a.C + c));
-      const float4 d = MODE == 1 ? __ldg(reinterpret_cast<const float4*>(a.dy + r * a.C + c)) : v;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
+      const float4 d = MODE == 1 ? __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)) : v;
       consume(v, d);
     }
   }
@@ -164,9 +181,8 @@ __global__ void __launch_bounds__(kThreads) bn_reduce_kernel(const BnArgs a) {
     red[1][threadIdx.x][j] = a1[j];
   }
   __syncthreads();
-  // block partial for this block's channels (row lanes summed in order)
-  const size_t slot = static_cast<size_t>(blockIdx.y * gridDim.x + blockIdx.x) * 2 * kBnGroup;
-  if (lane_r == 0) {
+  const int gx = gridDim.x;
+  if (lane_r == 0) {  // row lanes summed in order
     float t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
     for (int rr = 0; rr < rows_per_pass; ++rr) {
       const int src = rr * lanes + lane_c;
@@ -176,151 +192,185 @@ __global__ void __launch_bounds__(kThreads) bn_reduce_kernel(const BnArgs a) {
         t1[j] += red[1][src][j];
       }
     }
-    *reinterpret_cast<float4*>(a.w.part + slot + lane_c * 4) = make_float4(t0[0], t0[1], t0[2], t0[3]);
-    *reinterpret_cast<float4*>(a.w.part + slot + kBnGroup + lane_c * 4) =
-        make_float4(t1[0], t1[1], t1[2], t1[3]);
+    float* slot = a.w.part + static_cast<size_t>(blockIdx.y * gx + blockIdx.x) * 2 * kBnGroup;
+    *reinterpret_cast<float4*>(slot + lane_c * 4) = make_float4(t0[0], t0[1], t0[2], t0[3]);
+    *reinterpret_cast<float4*>(slot + kBnGroup + lane_c * 4) = make_float4(t1[0], t1[1], t1[2], t1[3]);
   }
-  const int ch_in_group = lanes * 4;
-  const int gx = gridDim.x;
-  // ---- level 1: the last block of this team sums the team's slots ----
-  const int team = blockIdx.y / kBnTeam;
-  const int team_lo = team * kBnTeam;
-  const int team_n = min(kBnTeam, static_cast<int>(gridDim.y) - team_lo);
-  unsigned* tcount = a.w.counters + kBnMaxGroups + blockIdx.x * kBnMaxTeams + team;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = (atomicAdd(tcount, 1u) == static_cast<unsigned>(team_n - 1));
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int v = threadIdx.x; v < 2 * kBnGroup; v += kThreads) {
-    if ((v & (kBnGroup - 1)) >= ch_in_group) continue;
-    float t = 0.f;
+
+  grid_barrier(a.w.counters, gridDim.x * gridDim.y);
+
+  // ---- phase 2: the group's Y slots, chunked over threads, fixed order ----
+  const int ch = lanes * 4;  // channels of this group
+  const int V = 2 * ch;      // values: sum1 of ch channels, then sum2
+  const int T = kBnThreads / V;
+  {
+    const int v = threadIdx.x % V;
+    const int chunk = threadIdx.x / V;
+    double t = 0.0;
+    if (chunk < T) {
+      const int y0 = chunk * a.Y / T, y1 = (chunk + 1) * a.Y / T;
+      const int off = v < ch ? v : kBnGroup + (v - ch);
 #pragma unroll 4
-    for (int y = team_lo; y < team_lo + team_n; ++y)
-      t += __ldcg(a.w.part + static_cast<size_t>(y * gx + blockIdx.x) * 2 * kBnGroup + v);
-    a.w.tpart[static_cast<size_t>(team * gx + blockIdx.x) * 2 * kBnGroup + v] = t;
+      for (int yy = y0; yy < y1; ++yy)
+        t += static_cast<double>(
+            __ldcg(a.w.part + static_cast<size_t>(yy * gx + blockIdx.x) * 2 * kBnGroup + off));
+    }
+    dsum[threadIdx.x] = t;
   }
-  if (threadIdx.x == 0) *tcount = 0u;  // re-arm
-  // ---- level 2: the last team of the channel group finalises ----
-  const int nteams = (gridDim.y + kBnTeam - 1) / kBnTeam;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0)
-    is_last = (atomicAdd(&a.w.counters[blockIdx.x], 1u) == static_cast<unsigned>(nteams - 1));
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int t = threadIdx.x; t < ch_in_group; t += kThreads) {
-    const int ch = blockIdx.x * ch_in_group + t;
-    if (ch >= a.C) continue;
+  if (threadIdx.x < ch) {
+    const int t = threadIdx.x;
     double s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
-    for (int tm = 0; tm < nteams; ++tm) {
-      const float* p = a.w.tpart + static_cast<size_t>(tm * gx + blockIdx.x) * 2 * kBnGroup;
-      s1 += static_cast<double>(__ldcg(p + t));
-      s2 += static_cast<double>(__ldcg(p + kBnGroup + t));
+    for (int k = 0; k < T; ++k) {
+      s1 += dsum[k * V + t];
+      s2 += dsum[k * V + ch + t];
     }
-    if (MODE == 0) {
-      const double mean = s1 / static_cast<double>(a.M);
-      double var = s2 / static_cast<double>(a.M) - mean * mean;
-      if (var < 0) var = 0;
-      const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(a.eps)));
-      const float sc = a.gamma[ch] * inv;
-      a.w.scale[ch] = sc;
-      a.w.shift[ch] = a.beta[ch] - static_cast<float>(mean) * sc;
-      if (a.save_mean) a.save_mean[ch] = static_cast<float>(mean);
-      if (a.save_invstd) a.save_invstd[ch] = inv;
-      if (a.run_mean && a.run_var && a.M > 1) {
-        const double unbiased = var * static_cast<double>(a.M) / static_cast<double>(a.M - 1);
-        a.run_mean[ch] = (1.f - a.momentum) * a.run_mean[ch] + a.momentum * static_cast<float>(mean);
-        a.run_var[ch] = (1.f - a.momentum) * a.run_var[ch] + a.momentum * static_cast<float>(unbiased);
+    const int chn = blockIdx.x * ch + t;
+    if (chn < a.C) {
+      if (MODE == 0) {
+        const double mean = s1 / static_cast<double>(a.M);
+        double var = s2 / static_cast<double>(a.M) - mean * mean;
+        if (var < 0) var = 0;
+        const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(a.eps)));
+        const float sc = a.gamma[chn] * inv;
+        coef[0][t] = sc;
+        coef[1][t] = a.beta[chn] - static_cast<float>(mean) * sc;
+        if (blockIdx.y == 0) {
+          if (a.save_mean) a.save_mean[chn] = static_cast<float>(mean);
+          if (a.save_invstd) a.save_invstd[chn] = inv;
+          if (a.run_mean && a.run_var && a.M > 1) {
+            const double unbiased = var * static_cast<double>(a.M) / static_cast<double>(a.M - 1);
+            a.run_mean[chn] = (1.f - a.momentum) * a.run_mean[chn] + a.momentum * static_cast<float>(mean);
+            a.run_var[chn] = (1.f - a.momentum) * a.run_var[chn] + a.momentum * static_cast<float>(unbiased);
+          }
+        }
+      } else {
+        const float invM = 1.f / static_cast<float>(a.M);
+        coef[0][t] = static_cast<float>(s1) * invM;  // mean(g)
+        coef[1][t] = static_cast<float>(s2) * invM;  // mean(g * xhat)
+        if (blockIdx.y == 0) {
+          if (a.dbeta) a.dbeta[chn] = static_cast<float>(s1);
+          if (a.dgamma) a.dgamma[chn] = static_cast<float>(s2);
+        }
       }
-    } else {
-      a.w.sum1[ch] = static_cast<float>(s1);
-      a.w.sum2[ch] = static_cast<float>(s2);
-      if (a.dbeta) a.dbeta[ch] = static_cast<float>(s1);
-      if (a.dgamma) a.dgamma[ch] = static_cast<float>(s2);
     }
   }
-  if (threadIdx.x == 0) a.w.counters[blockIdx.x] = 0u;  // re-arm for the next launch
-}
+  __syncthreads();
 
-__global__ void __launch_bounds__(kThreads) bn_apply_kernel(
-    const float* __restrict__ x, long long total4, int C4, const float* __restrict__ scale,
-    const float* __restrict__ shift, int relu, float* __restrict__ y) {
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total4;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % C4) * 4;
-    float4 v = reinterpret_cast<const float4*>(x)[i];
-    const float4 sc = *reinterpret_cast<const float4*>(scale + c);
-    const float4 sh = *reinterpret_cast<const float4*>(shift + c);
-    v.x = v.x * sc.x + sh.x;
-    v.y = v.y * sc.y + sh.y;
-    v.z = v.z * sc.z + sh.z;
-    v.w = v.w * sc.w + sh.w;
-    if (relu) {
-      v.x = fmaxf(v.x, 0.f);
-      v.y = fmaxf(v.y, 0.f);
-      v.z = fmaxf(v.z, 0.f);
-      v.w = fmaxf(v.w, 0.f);
+  // ---- phase 3: the block's rows again ----
+  if (!c_ok) return;
+  const int cl = lane_c * 4;
+  if (MODE == 0) {
+    const float sc[4] = {coef[0][cl], coef[0][cl + 1], coef[0][cl + 2], coef[0][cl + 3]};
+    const float sh[4] = {coef[1][cl], coef[1][cl + 1], coef[1][cl + 2], coef[1][cl + 3]};
+    auto f = [&](float4 v) {
+      v.x = v.x * sc[0] + sh[0];
+      v.y = v.y * sc[1] + sh[1];
+      v.z = v.z * sc[2] + sh[2];
+      v.w = v.w * sc[3] + sh[3];
+      if (a.relu) {
+        v.x = fmaxf(v.x, 0.f);
+        v.y = fmaxf(v.y, 0.f);
+        v.z = fmaxf(v.z, 0.f);
+        v.w = fmaxf(v.w, 0.f);
+      }
+      return v;
+    };
+    long long r = r_begin + lane_r;
+    for (; r + 3 * step < r_end; r += 4 * step) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) *reinterpret_cast<float4*>(a.y + (r + u * step) * C + c) = f(v[u]);
     }
-    reinterpret_cast<float4*>(y)[i] = v;
-  }
-}
-
-// dx = gamma*invstd * (g - mean(g) - xhat * mean(g*xhat))
-__global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(
-    const float* __restrict__ x, const float* __restrict__ dy, long long total4, int C4,
-    long long M, const float* __restrict__ gamma, const float* __restrict__ beta,
-    const float* __restrict__ mean, const float* __restrict__ invstd,
-    const float* __restrict__ s1, const float* __restrict__ s2, int relu,
-    float* __restrict__ dx, int dx_beta) {
-  const float invM = 1.f / static_cast<float>(M);
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total4;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % C4) * 4;
-    const float4 xv4 = reinterpret_cast<const float4*>(x)[i];
-    const float4 dv4 = reinterpret_cast<const float4*>(dy)[i];
-    const float xv[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
-    const float dv[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
-    float o[4];
+    for (; r < r_end; r += step)
+      *reinterpret_cast<float4*>(a.y + r * C + c) = f(__ldg(reinterpret_cast<const float4*>(a.x + r * C + c)));
+  } else {
+    float mg[4], mgx[4], k0[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float is = invstd[c + j], ga = gamma[c + j];
-      const float xh = (xv[j] - mean[c + j]) * is;
-      float g = dv[j];
-      if (relu && (xh * ga + beta[c + j]) <= 0.f) g = 0.f;
-      const float mg = s1[c + j] * invM;
-      const float mgx = s2[c + j] * invM;
-      o[j] = ga * is * (g - mg - xh * mgx);
+      mg[j] = coef[0][cl + j];
+      mgx[j] = coef[1][cl + j];
+      k0[j] = ga[j] * is[j];
     }
-    float4 r = make_float4(o[0], o[1], o[2], o[3]);
-    if (dx_beta) {
-      const float4 old = reinterpret_cast<float4*>(dx)[i];
-      r.x += old.x;
-      r.y += old.y;
-      r.z += old.z;
-      r.w += old.w;
+    auto f = [&](const float4 xv4, const float4 dv4, long long r) {
+      const float xv[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
+      const float dv[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+      float o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float xh = (xv[j] - mu[j]) * is[j];
+        float g = dv[j];
+        if (a.relu && (xh * ga[j] + be[j]) <= 0.f) g = 0.f;
+        o[j] = k0[j] * (g - mg[j] - xh * mgx[j]);
+      }
+      float4 out = make_float4(o[0], o[1], o[2], o[3]);
+      float4* d = reinterpret_cast<float4*>(a.dx + r * C + c);
+      if (a.dx_beta) {
+        const float4 old = *d;
+        out.x += old.x;
+        out.y += old.y;
+        out.z += old.z;
+        out.w += old.w;
+      }
+      *d = out;
+    };
+    long long r = r_begin + lane_r;
+    for (; r + 3 * step < r_end; r += 4 * step) {
+      float4 xv[4], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xv[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
+        dv[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * C + c));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], r + u * step);
     }
-    reinterpret_cast<float4*>(dx)[i] = r;
+    for (; r < r_end; r += step)
+      f(__ldg(reinterpret_cast<const float4*>(a.x + r * C + c)),
+        __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)), r);
   }
 }
 
-// grid of the reduction: channel groups of lanes*4 <= 128 channels, Y row
-// splits so that x*Y ~ 4 blocks per SM (<= kBnMaxBlocks), >= 32 rows each
-void bn_reduce_launch_dims(long long M, int C, int* lanes, dim3* grid) {
-  int l = C / 4;
+// cooperative grid: channel groups of lanes*4 <= 128 channels x Y row splits,
+// all blocks co-resident (the occupancy limit), ~2 blocks per SM, >= 16 rows
+// per block, Y <= kBnMaxY
+template <int MODE>
+int bn_launch(BnArgs a, cudaStream_t st) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<MODE>, kBnThreads, 0);
+    if (occ < 1) occ = 1;
+  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);
+  int l = a.C / 4;
   if (l > kBnGroup / 4) l = kBnGroup / 4;
   if (l < 1) l = 1;
-  *lanes = l;
-  const int cgroups = (C / 4 + l - 1) / l;
-  long long y = (148LL * 4 + cgroups - 1) / cgroups;
-  const long long max_y = (M + 31) / 32;
-  if (y > max_y) y = max_y;
-  if (y > kBnMaxBlocks / cgroups) y = kBnMaxBlocks / cgroups;
+  a.lanes = l;
+  const int gx = (a.C / 4 + l - 1) / l;
+  if (gx > max_blocks) return static_cast<int>(cudaErrorInvalidConfiguration);
+  long long y = (2LL * sms + gx - 1) / gx;
+  y = std::min<long long>(y, (a.M + 15) / 16);
+  y = std::min<long long>(y, kBnMaxY);
+  y = std::min<long long>(y, max_blocks / gx);
   if (y < 1) y = 1;
-  *grid = dim3(cgroups, static_cast<unsigned>(y));
+  a.Y = static_cast<int>(y);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gx, a.Y);
+  cfg.blockDim = dim3(kBnThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE>, a));
 }
 
 // ---------------------------------------------------------------------------
@@ -328,6 +378,8 @@ void bn_reduce_launch_dims(long long M, int C, int* lanes, dim3* grid) {
 // ---------------------------------------------------------------------------
 __global__ void relu_fwd_kernel(const float4* __restrict__ x, float4* __restrict__ y,
                                 long long n4) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float4 v = x[i];
@@ -341,6 +393,8 @@ __global__ void relu_fwd_kernel(const float4* __restrict__ x, float4* __restrict
 
 __global__ void relu_bwd_kernel(const float4* __restrict__ x, const float4* __restrict__ dy,
                                 float4* __restrict__ dx, long long n4, int beta) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const float4 v = x[i];
@@ -360,6 +414,8 @@ __global__ void relu_bwd_kernel(const float4* __restrict__ x, const float4* __re
 
 __global__ void add_kernel(const float4* __restrict__ a, const float4* __restrict__ b,
                            float4* __restrict__ y, long long n4) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const float4 u = a[i], v = b[i];
@@ -369,6 +425,8 @@ __global__ void add_kernel(const float4* __restrict__ a, const float4* __restric
 
 __global__ void copy_kernel(const float4* __restrict__ s, float4* __restrict__ d, long long n4,
                             int beta) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float4 v = s[i];
@@ -389,6 +447,8 @@ __global__ void copy_kernel(const float4* __restrict__ s, float4* __restrict__ d
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int n, int h, int w, int c4,
                                    int kr, int ks, int stride, int pad, int p, int q,
                                    float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = static_cast<long long>(n) * p * q * c4;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -423,6 +483,8 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int n, int h, in
 __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy,
                                    int n, int h, int w, int c4, int kr, int ks, int stride,
                                    int pad, int p, int q, float* __restrict__ dx) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = static_cast<long long>(n) * h * w * c4;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   const float4* dy4 = reinterpret_cast<const float4*>(dy);
@@ -476,8 +538,91 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __r
   }
 }
 
+// two-pass max-pool backward: (1) the argmax tap (row-major first maximum)
+// of every output window and channel as one byte; (2) every input element
+// gathers dy over the <= ceil(k/stride)^2 windows covering it whose argmax
+// is this element, in window order (deterministic).
+__global__ void maxpool_argmax_kernel(const float* __restrict__ x, int n, int h, int w, int c4,
+                                      int kr, int ks, int stride, int pad, int p, int q,
+                                      uint8_t* __restrict__ arg, int total) {
+  pdl_wait();
+  pdl_trigger();
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, channel float4)
+  if (idx >= total) return;
+  const int cg = idx % c4;
+  const int pix = idx / c4;  // (n, pp, qq)
+  const int qq = pix % q;
+  const int pp = (pix / q) % p;
+  const int nn = pix / (p * q);
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  int bt[4] = {0, 0, 0, 0};
+  for (int r = 0; r < kr; ++r) {
+    const int ih = pp * stride - pad + r;
+    if (ih < 0 || ih >= h) continue;
+    for (int s = 0; s < ks; ++s) {
+      const int iw = qq * stride - pad + s;
+      if (iw < 0 || iw >= w) continue;
+      const float4 v = __ldg(x4 + ((static_cast<long long>(nn) * h + ih) * w + iw) * c4 + cg);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (vv[j] > best[j]) {
+          best[j] = vv[j];
+          bt[j] = r * ks + s;
+        }
+    }
+  }
+  const uint32_t packed = static_cast<uint32_t>(bt[0]) | (static_cast<uint32_t>(bt[1]) << 8) |
+                          (static_cast<uint32_t>(bt[2]) << 16) | (static_cast<uint32_t>(bt[3]) << 24);
+  reinterpret_cast<uint32_t*>(arg)[static_cast<long long>(pix) * c4 + cg] = packed;
+}
+
+__global__ void maxpool_gather_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
+                                      int n, int h, int w, int c4, int kr, int ks, int stride,
+                                      int pad, int p, int q, float* __restrict__ dx, int total) {
+  pdl_wait();
+  pdl_trigger();
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, channel float4)
+  if (idx >= total) return;
+  const int cg = idx % c4;
+  const int pix = idx / c4;  // (n, hh, ww)
+  const int ww = pix % w;
+  const int hh = (pix / w) % h;
+  const int nn = pix / (w * h);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int p_lo = max(0, (hh + pad - kr + stride) / stride);
+  const int p_hi = min(p - 1, (hh + pad) / stride);
+  const int q_lo = max(0, (ww + pad - ks + stride) / stride);
+  const int q_hi = min(q - 1, (ww + pad) / stride);
+  const uint32_t* a32 = reinterpret_cast<const uint32_t*>(arg);
+  const float4* dy4 = reinterpret_cast<const float4*>(dy);
+  for (int pp = p_lo; pp <= p_hi; ++pp) {
+    for (int qq = q_lo; qq <= q_hi; ++qq) {
+      const int tap = (hh - (pp * stride - pad)) * ks + (ww - (qq * stride - pad));
+      const long long o = (static_cast<long long>(nn) * p + pp) * q + qq;
+      const uint32_t packed = __ldg(a32 + o * c4 + cg);
+      const bool hit[4] = {(packed & 0xFF) == static_cast<uint32_t>(tap),
+                           ((packed >> 8) & 0xFF) == static_cast<uint32_t>(tap),
+                           ((packed >> 16) & 0xFF) == static_cast<uint32_t>(tap),
+                           (packed >> 24) == static_cast<uint32_t>(tap)};
+      if (hit[0] || hit[1] || hit[2] || hit[3]) {
+        const float4 g = __ldg(dy4 + o * c4 + cg);
+        if (hit[0]) acc[0] += g.x;
+        if (hit[1]) acc[1] += g.y;
+        if (hit[2]) acc[2] += g.z;
+        if (hit[3]) acc[3] += g.w;
+      }
+    }
+  }
+  reinterpret_cast<float4*>(dx)[static_cast<long long>(pix) * c4 + cg] =
+      make_float4(acc[0], acc[1], acc[2], acc[3]);
+}
+
 __global__ void avgpool_fwd_kernel(const float* __restrict__ x, int n, int hw, int c,
                                    float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int total = n * c;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int nn = i / c, cc = i - nn * c;
@@ -488,22 +633,31 @@ __global__ void avgpool_fwd_kernel(const float* __restrict__ x, int n, int hw, i
   }
 }
 
+// dx[n][j][c] = dy[n][c] / hw; grid (channel float4 blocks, n * hw pixels)
 __global__ void avgpool_bwd_kernel(const float* __restrict__ dy, int n, int hw, int c,
                                    float* __restrict__ dx) {
-  const long long total = static_cast<long long>(n) * hw * c;
+  pdl_wait();
+  pdl_trigger();
+  const int c4 = c / 4;
+  const int cg = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cg >= c4) return;
+  const int pix = blockIdx.y;  // n * hw + j
+  const int nn = pix / hw;
   const float inv = 1.f / static_cast<float>(hw);
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int cc = static_cast<int>(i % c);
-    const long long nn = i / (static_cast<long long>(hw) * c);
-    dx[i] = dy[nn * c + cc] * inv;
-  }
+  float4 g = reinterpret_cast<const float4*>(dy)[static_cast<long long>(nn) * c4 + cg];
+  g.x *= inv;
+  g.y *= inv;
+  g.z *= inv;
+  g.w *= inv;
+  reinterpret_cast<float4*>(dx)[static_cast<long long>(pix) * c4 + cg] = g;
 }
 
 // ---------------------------------------------------------------------------
 // classifier
 // ---------------------------------------------------------------------------
 __global__ void bias_add_kernel(float* y, const float* b, long long m, int n) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = m * n;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -526,6 +680,8 @@ constexpr int kXentThreads = 1024;
 __global__ void __launch_bounds__(kXentThreads) xent_kernel(
     const float* __restrict__ logits, const int* __restrict__ labels, int rows, int classes,
     float* loss, float* dlogits, float* dbias) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float row_loss[kXentThreads / 32];
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -570,6 +726,8 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(
 __global__ void sgd_kernel(float4* __restrict__ w, const float4* __restrict__ g,
                            float4* __restrict__ buf, long long n4, float lr, float mu, float wd,
                            float gscale, int first) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float4 wv = w[i];
@@ -596,6 +754,8 @@ __global__ void sgd_kernel(float4* __restrict__ w, const float4* __restrict__ g,
 
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, int n, int c, int h, int w,
                                     int c4, float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = static_cast<long long>(n) * h * w * c4;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -614,9 +774,14 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, int n, int c, i
 
 using namespace accudnn;
 
+extern "C" int accudnn_set_pdl(int enable) {
+  const int prev = accudnn::g_pdl;
+  accudnn::g_pdl = enable ? 1 : 0;
+  return prev;
+}
+
 extern "C" unsigned long long accudnn_bn_workspace_bytes(int C) {
-  return sizeof(float) * (2ull * kBnMaxBlocks * 2 * kBnGroup + 4ull * C) +
-         sizeof(unsigned) * kBnCounters;
+  return sizeof(unsigned) * kBnCounters + sizeof(float) * 2ull * kBnMaxBlocks * kBnGroup;
 }
 
 extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* gamma,
@@ -624,12 +789,11 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
                               float* save_mean, float* save_invstd, float* running_mean,
                               float* running_var, float momentum, void* ws, void* stream) {
   if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
-  const BnWs w = bn_ws(ws, C);
-  cudaStream_t st = S(stream);
   BnArgs a{};
   a.x = x;
   a.M = M;
   a.C = C;
+  a.relu = relu;
   a.gamma = gamma;
   a.beta = beta;
   a.eps = eps;
@@ -638,15 +802,9 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
   a.save_invstd = save_invstd;
   a.run_mean = running_mean;
   a.run_var = running_var;
-  a.w = w;
-  dim3 grid;
-  bn_reduce_launch_dims(M, C, &a.lanes, &grid);
-  a.Y = static_cast<int>(grid.y);
-  bn_reduce_kernel<0><<<grid, kThreads, 0, st>>>(a);
-  const long long total4 = M * C / 4;
-  bn_apply_kernel<<<grid_for(total4, kThreads), kThreads, 0, st>>>(x, total4, C / 4, w.scale,
-                                                                   w.shift, relu, y);
-  return static_cast<int>(cudaGetLastError());
+  a.y = y;
+  a.w = bn_ws(ws, C);
+  return bn_launch<0>(a, S(stream));
 }
 
 extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int C,
@@ -654,8 +812,6 @@ extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int 
                               const float* save_invstd, int relu, float* dx, int dx_beta,
                               float* dgamma, float* dbeta, void* ws, void* stream) {
   if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
-  const BnWs w = bn_ws(ws, C);
-  cudaStream_t st = S(stream);
   BnArgs a{};
   a.x = x;
   a.dy = dy;
@@ -668,21 +824,15 @@ extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int 
   a.invstd = save_invstd;
   a.dgamma = dgamma;
   a.dbeta = dbeta;
-  a.w = w;
-  dim3 grid;
-  bn_reduce_launch_dims(M, C, &a.lanes, &grid);
-  a.Y = static_cast<int>(grid.y);
-  bn_reduce_kernel<1><<<grid, kThreads, 0, st>>>(a);
-  const long long total4 = M * C / 4;
-  bn_bwd_dx_kernel<<<grid_for(total4, kThreads), kThreads, 0, st>>>(
-      x, dy, total4, C / 4, M, gamma, beta, save_mean, save_invstd, w.sum1, w.sum2, relu, dx,
-      dx_beta);
-  return static_cast<int>(cudaGetLastError());
+  a.dx = dx;
+  a.dx_beta = dx_beta;
+  a.w = bn_ws(ws, C);
+  return bn_launch<1>(a, S(stream));
 }
 
 extern "C" int accudnn_relu_fwd(const float* x, float* y, long long n, void* stream) {
   if (n & 3) return static_cast<int>(cudaErrorInvalidValue);
-  relu_fwd_kernel<<<grid_for(n / 4, kThreads), kThreads, 0, S(stream)>>>(
+  launch_pdl(relu_fwd_kernel, grid_for(n / 4, kThreads), kThreads, 0, S(stream), 
       reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), n / 4);
   return static_cast<int>(cudaGetLastError());
 }
@@ -690,7 +840,7 @@ extern "C" int accudnn_relu_fwd(const float* x, float* y, long long n, void* str
 extern "C" int accudnn_relu_bwd(const float* x, const float* dy, float* dx, long long n,
                                 int dx_beta, void* stream) {
   if (n & 3) return static_cast<int>(cudaErrorInvalidValue);
-  relu_bwd_kernel<<<grid_for(n / 4, kThreads), kThreads, 0, S(stream)>>>(
+  launch_pdl(relu_bwd_kernel, grid_for(n / 4, kThreads), kThreads, 0, S(stream), 
       reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
       reinterpret_cast<float4*>(dx), n / 4, dx_beta);
   return static_cast<int>(cudaGetLastError());
@@ -699,7 +849,7 @@ extern "C" int accudnn_relu_bwd(const float* x, const float* dy, float* dx, long
 extern "C" int accudnn_add_fwd(const float* a, const float* b, float* y, long long n,
                                void* stream) {
   if (n & 3) return static_cast<int>(cudaErrorInvalidValue);
-  add_kernel<<<grid_for(n / 4, kThreads), kThreads, 0, S(stream)>>>(
+  launch_pdl(add_kernel, grid_for(n / 4, kThreads), kThreads, 0, S(stream), 
       reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(b),
       reinterpret_cast<float4*>(y), n / 4);
   return static_cast<int>(cudaGetLastError());
@@ -707,7 +857,7 @@ extern "C" int accudnn_add_fwd(const float* a, const float* b, float* y, long lo
 
 extern "C" int accudnn_copy(const float* src, float* dst, long long n, int beta, void* stream) {
   if (n & 3) return static_cast<int>(cudaErrorInvalidValue);
-  copy_kernel<<<grid_for(n / 4, kThreads), kThreads, 0, S(stream)>>>(
+  launch_pdl(copy_kernel, grid_for(n / 4, kThreads), kThreads, 0, S(stream), 
       reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), n / 4, beta);
   return static_cast<int>(cudaGetLastError());
 }
@@ -716,7 +866,7 @@ extern "C" int accudnn_maxpool_fwd(const float* x, int n, int h, int w, int c, i
                                    int stride, int pad, int p, int q, float* y, void* stream) {
   if (c & 3) return static_cast<int>(cudaErrorInvalidValue);
   const long long total = static_cast<long long>(n) * p * q * (c / 4);
-  maxpool_fwd_kernel<<<grid_for(total, kThreads), kThreads, 0, S(stream)>>>(
+  launch_pdl(maxpool_fwd_kernel, grid_for(total, kThreads), kThreads, 0, S(stream), 
       x, n, h, w, c / 4, kr, ks, stride, pad, p, q, y);
   return static_cast<int>(cudaGetLastError());
 }
@@ -725,41 +875,58 @@ extern "C" int accudnn_maxpool_bwd(const float* x, const float* dy, int n, int h
                                    int kr, int ks, int stride, int pad, int p, int q, float* dx,
                                    void* stream) {
   if (c & 3) return static_cast<int>(cudaErrorInvalidValue);
-  const long long total = static_cast<long long>(n) * h * w * (c / 4);
-  maxpool_bwd_kernel<<<grid_for(total, kThreads), kThreads, 0, S(stream)>>>(
-      x, dy, n, h, w, c / 4, kr, ks, stride, pad, p, q, dx);
+  const int c4 = c / 4;
+  // argmax bytes live in the convolution split-K workspace (idle between
+  // convolutions on this stream); without one, the single-pass kernel
+  const long long in4 = static_cast<long long>(n) * h * w * c4;
+  const long long out4 = static_cast<long long>(n) * p * q * c4;
+  uint8_t* arg = (kr * ks <= 256 && in4 < (1LL << 31) && out4 < (1LL << 31))
+                     ? reinterpret_cast<uint8_t*>(
+                           conv_splitk_workspace(static_cast<size_t>(n) * p * q * c))
+                     : nullptr;
+  if (arg) {
+    launch_pdl(maxpool_argmax_kernel, static_cast<unsigned>((out4 + 255) / 256), 256, 0,
+               S(stream), x, n, h, w, c4, kr, ks, stride, pad, p, q, arg, static_cast<int>(out4));
+    launch_pdl(maxpool_gather_kernel, static_cast<unsigned>((in4 + 255) / 256), 256, 0,
+               S(stream), arg, dy, n, h, w, c4, kr, ks, stride, pad, p, q, dx,
+               static_cast<int>(in4));
+    return static_cast<int>(cudaGetLastError());
+  }
+  const long long total = static_cast<long long>(n) * h * w * c4;
+  launch_pdl(maxpool_bwd_kernel, grid_for(total, kThreads), kThreads, 0, S(stream), x, dy, n, h,
+             w, c4, kr, ks, stride, pad, p, q, dx);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int accudnn_avgpool_fwd(const float* x, int n, int hw, int c, float* y,
                                    void* stream) {
-  avgpool_fwd_kernel<<<grid_for(static_cast<long long>(n) * c, kThreads), kThreads, 0,
-                       S(stream)>>>(x, n, hw, c, y);
+  launch_pdl(avgpool_fwd_kernel, grid_for(static_cast<long long>(n) * c, kThreads), kThreads, 0, S(stream), x, n, hw, c, y);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int accudnn_avgpool_bwd(const float* dy, int n, int hw, int c, float* dx,
                                    void* stream) {
-  avgpool_bwd_kernel<<<grid_for(static_cast<long long>(n) * hw * c, kThreads), kThreads, 0,
-                       S(stream)>>>(dy, n, hw, c, dx);
+  if (c & 3) return static_cast<int>(cudaErrorInvalidValue);
+  launch_pdl(avgpool_bwd_kernel, dim3((c / 4 + 127) / 128, static_cast<unsigned>(n * hw)), 128, 0,
+             S(stream), dy, n, hw, c, dx);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int accudnn_bias_add(float* y, const float* bias, long long m, int n, void* stream) {
-  bias_add_kernel<<<grid_for(m * n, kThreads), kThreads, 0, S(stream)>>>(y, bias, m, n);
+  launch_pdl(bias_add_kernel, grid_for(m * n, kThreads), kThreads, 0, S(stream), y, bias, m, n);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int accudnn_xent_fwd(const float* logits, const int* labels, int rows, int classes,
                                 float* loss, void* stream) {
-  xent_kernel<<<1, kXentThreads, 0, S(stream)>>>(logits, labels, rows, classes, loss, nullptr,
+  launch_pdl(xent_kernel, 1, kXentThreads, 0, S(stream), logits, labels, rows, classes, loss, nullptr,
                                                  nullptr);
   return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int accudnn_xent_bwd(const float* logits, const int* labels, int rows, int classes,
                                 float* dlogits, float* dbias, void* stream) {
-  xent_kernel<<<1, kXentThreads, 0, S(stream)>>>(logits, labels, rows, classes, nullptr,
+  launch_pdl(xent_kernel, 1, kXentThreads, 0, S(stream), logits, labels, rows, classes, nullptr,
                                                  dlogits, dbias);
   return static_cast<int>(cudaGetLastError());
 }
@@ -768,7 +935,7 @@ extern "C" int accudnn_sgd_update(float* w, const float* g, float* buf, long lon
                                   float momentum, float weight_decay, float grad_scale,
                                   int first_step, void* stream) {
   if (n & 3) return static_cast<int>(cudaErrorInvalidValue);
-  sgd_kernel<<<grid_for(n / 4, kThreads), kThreads, 0, S(stream)>>>(
+  launch_pdl(sgd_kernel, grid_for(n / 4, kThreads), kThreads, 0, S(stream), 
       reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(g),
       reinterpret_cast<float4*>(buf), n / 4, lr, momentum, weight_decay, grad_scale,
       first_step);
@@ -778,7 +945,7 @@ extern "C" int accudnn_sgd_update(float* w, const float* g, float* buf, long lon
 extern "C" int accudnn_nchw_to_nhwc_pad(const float* x, int n, int c, int h, int w, int c4,
                                         float* y, void* stream) {
   const long long total = static_cast<long long>(n) * h * w * c4;
-  nchw_to_nhwc_kernel<<<grid_for(total, kThreads), kThreads, 0, S(stream)>>>(x, n, c, h, w, c4,
+  launch_pdl(nchw_to_nhwc_kernel, grid_for(total, kThreads), kThreads, 0, S(stream), x, n, c, h, w, c4,
                                                                             y);
   return static_cast<int>(cudaGetLastError());
 }

@@ -156,6 +156,7 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaMallocHost(&I.loss_host, sizeof(float)), "loss host");
   if (conv_ws) ck(cudaMalloc(&I.conv_ws, conv_ws), "conv workspace");
   ckl(accudnn_conv_set_workspace(I.conv_ws, I.conv_ws ? conv_ws : 0), "conv workspace");
+  if (cfg.autotune) accudnn_conv_autotune(1);
   ck(cudaMemset(I.params, 0, pbytes), "memset");
   ck(cudaMemset(I.grads, 0, pbytes), "memset");
   ck(cudaMemset(I.momentum_buf, 0, pbytes), "memset");
@@ -485,9 +486,13 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       }
       for (int o : ops) {
         const Op& op = net.ops[static_cast<size_t>(o)];
-        for (int x : {op.in0, op.in1})
-          if (x >= 0 && I.swapped[static_cast<size_t>(x)] && !fwd)
-            ck(cudaStreamWaitEvent(cs, I.h2d_done[static_cast<size_t>(x)], 0), "wait");
+        // only inputs the backward actually reads were prefetched for it (an
+        // add's backward reads none; waiting there would reference the
+        // previous iteration's prefetch, which stream capture rejects)
+        if (!fwd && bwd_reads_input(op))
+          for (int x : {op.in0, op.in1})
+            if (x >= 0 && I.swapped[static_cast<size_t>(x)])
+              ck(cudaStreamWaitEvent(cs, I.h2d_done[static_cast<size_t>(x)], 0), "wait");
       }
       for (int inst : I.first_compute_write[static_cast<size_t>(s)]) wait_region(inst, cs, true);
       if (profile && !capture) ck(cudaEventRecord(I.phase_begin[static_cast<size_t>(s)], cs), "rec");

@@ -42,6 +42,7 @@ struct ExecConfig {
   float bn_momentum = 0.1f;
   int device = 0;
   long long bucket_bytes = 25LL << 20;
+  int autotune = 1;                // tune conv tile/split-K per shape in the first (eager) step
 };
 
 struct StepStats {

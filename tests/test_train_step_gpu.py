@@ -156,3 +156,24 @@ def test_cuda_graph_step_matches_eager(cuda_dev):
         lb = b.step(x, y, lr=0.05)["loss"]
         assert la == lb
     assert np.array_equal(b.get_params(), a.get_params())
+
+
+def test_cuda_graph_with_swap_plan_matches_eager(cuda_dev):
+    """the captured iteration (kernels + D2H offloads + H2D prefetches + event
+    edges) of a swapping plan computes exactly what the eager iteration does."""
+    arch, image, classes, k = "resnet50", 64, 8, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    n = len(desc["ops"])
+    plan = json.dumps({"k_star": k, "pinned_objects": [f"fm{l}" for l in range(1, n + 1, 4)]})
+    params = trainer.init_params(desc, seed=6)
+    a = trainer.Executor(arch, image, classes, k=k, mode="dynamic", plan_json=plan)
+    b = trainer.Executor(arch, image, classes, k=k, mode="dynamic", plan_json=plan)
+    a.set_params(params)
+    b.set_params(params)
+    b.set_graph(True)
+    for it in range(3):
+        x, y = data(k, image, classes, seed=30 + it)
+        la = a.step(x, y, lr=0.05)["loss"]
+        lb = b.step(x, y, lr=0.05)["loss"]
+        assert la == lb
+    assert np.array_equal(b.get_params(), a.get_params())

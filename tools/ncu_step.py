@@ -1,4 +1,5 @@
-"""One eager ResNet training step for ncu (launch list / full capture).
+"""One eager ResNet training step for ncu (launch list / full capture), after
+warm-up steps, bracketed by cudaProfilerStart/Stop.
 Usage: python tools/ncu_step.py [arch] [k] [warmup]"""
 import os
 import sys
@@ -20,7 +21,14 @@ ex.set_params(trainer.init_params(desc, 0))
 g = np.random.default_rng(0)
 x = torch.from_numpy(g.standard_normal((k, 3, image, image)).astype(np.float32)).cuda()
 y = torch.from_numpy(g.integers(0, classes, size=k).astype(np.int32)).cuda()
-for _ in range(warm + 1):
-    out = ex.step(x, y, lr=0.01)
+# warm-up steps (the first one autotunes the conv kernels), then exactly one
+# profiled step between cudaProfilerStart/Stop (run ncu with
+# --profile-from-start off)
+for _ in range(max(1, warm)):
+    ex.step(x, y, lr=0.01)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
+out = ex.step(x, y, lr=0.01)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("step done", out)
