@@ -45,6 +45,9 @@ int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes);
 /* programmatic dependent launch for every kernel (default 0): the next
  * kernel's prologue overlaps the previous one's tail.  Returns the previous. */
 int accudnn_set_pdl(int enable);
+/* debug: TMA-conv launches record per-CTA clock64 stamps into buf (1024 x
+ * int64 per CTA, see conv_sm100.cu); NULL turns it off */
+int accudnn_conv_trace(void* buf);
 /* 1: tune (tile width, split-K) per convolution shape on its first
  * overwrite (beta = 0) call outside stream capture -- every candidate is
  * timed with CUDA events and the fastest is cached for the process; 0: the

@@ -113,6 +113,7 @@ CUDA_SYMBOLS = {
     "accudnn_conv_set_workspace": ([ctypes.c_void_p, ctypes.c_ulonglong], _I),
     "accudnn_conv_autotune": ([_I], _I),
     "accudnn_set_pdl": ([_I], _I),
+    "accudnn_conv_trace": ([_P], _I),
     "accudnn_conv_fwd": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_dgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_wgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _I, _P], _I),

@@ -73,6 +73,8 @@ struct Prob {
   float* out;
   int beta;
   float* ws;           // split-K partials [split][M][Ng]
+  long long* trace;    // debug: per-CTA clock64 stamps (accudnn_conv_trace), or nullptr
+  int tma_out;         // epilogue stores through tmC (bulk tensor stores / reduce-adds)
 };
 
 // ---- TMA PTX -------------------------------------------------------------------
@@ -106,6 +108,46 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// smem -> global bulk tensor store (or element-wise add into global), 2-D
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tm)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, uint32_t src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tm)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* tm, uint32_t src, int c0,
+                                                  int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tm)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N bulk groups still reading their smem source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
 }
@@ -126,7 +168,8 @@ __device__ __forceinline__ long long out_row(const Prob& a, int m) {
 template <int MODE, int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, const Prob a) {
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, const Prob a) {
   constexpr bool kAmn = (MODE == WGRAD);
   constexpr bool kBmn = (MODE != FWD);
   constexpr uint32_t kABytes = kBM * kBK * 4;
@@ -145,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 768] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -158,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (a.tma_out) prefetch_tmap(&tmC);
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
@@ -168,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // everything above overlapped the previous kernel's tail (PDL)
   pdl_wait();
   pdl_trigger();
+  if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 769] = gtimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -201,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++kc) {
           const uint32_t stage = kc % STAGES;
           if (kc >= STAGES) ptx::mbar_wait(&empty[stage], ((kc / STAGES) - 1) & 1);
+          if (a.trace && kc < 256) a.trace[blockIdx.x * 1024 + kc] = clock64();
           const uint32_t sA = smem_base + stage * kStageBytes;
           const uint32_t sB = sA + kABytes;
           uint64_t* bar = &full[stage];
@@ -261,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++kc) {
           const uint32_t stage = kc % STAGES;
           ptx::mbar_wait(&full[stage], (kc / STAGES) & 1);
+          if (a.trace && kc < 256) a.trace[blockIdx.x * 1024 + 256 + kc] = clock64();
           ptx::tc_fence_after();
           const uint32_t sA = smem_base + stage * kStageBytes;
           const uint32_t sB = sA + kABytes;
@@ -279,17 +327,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ============================ epilogue ============================
-    // Each warp drains its TMEM lane quadrant (32 rows) in 32-column chunks:
-    // tcgen05.ld -> registers -> a private 4 KB smem transpose buffer (16-byte
-    // granules XOR-swizzled by row) -> coalesced 128-byte row segments to HBM
-    // (4 rows per instruction).  With split-K the chunk goes to the slice's
-    // workspace rows instead; conv_splitk_reduce_kernel sums the slices.
+    // Each warp drains its TMEM lane quadrant (32 rows) in 32-column chunks.
+    // TMA-store path (row-major outputs and split-K slices): tcgen05.ld ->
+    // registers -> one of two 4 KB smem buffers in the SWIZZLE_128B layout
+    // -> one bulk tensor store (or element-wise add for beta = 1) issued by
+    // lane 0, which completes asynchronously while the next chunk is
+    // staged in the other buffer.  Scatter outputs (strided dgrad classes) use coalesced
+    // 128-byte row segments from the same smem transpose instead.
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    const int ew = warp - 2;    // staging buffer of this warp
-    float* stage_buf = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 1024) + ew * 1024;
-    const uint32_t sbuf = ptx::smem_u32(stage_buf);
-    const int rr_lo = lane >> 3;  // read-back row within a group of 4
+    const int ew = warp - 2;    // staging buffers of this warp
+    float* stage_buf = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 1024) + ew * 2048;
+    const uint32_t sbuf0 = ptx::smem_u32(stage_buf);
+    const int rr_lo = lane >> 3;  // read-back row within a group of 4 (scatter path)
     const int gg = lane & 7;      // read-back 16-byte granule
+    uint32_t nchunk = 0;          // chunks staged by this warp (buffer parity)
     int j = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++j) {
       const int split = u % a.splits;
@@ -299,73 +350,82 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = tm * kBM + quad * 32, n0 = tn * BN;
       const int acc = j & 1;
       ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      if (a.trace && threadIdx.x == 64 && j < 128) a.trace[blockIdx.x * 1024 + 512 + 2 * j] = clock64();
       ptx::tc_fence_after();
       const uint32_t trow = tmem + static_cast<uint32_t>(acc * BN) +
                             (static_cast<uint32_t>(quad * 32) << 16);
       const int ncols = min(BN, a.Ng - n0);  // multiple of 4
       const bool partial = a.splits > 1;
-      // destination row offsets of the 4 x 8 rows this lane writes
-      long long drow[8];
-#pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int m = m0 + it * 4 + rr_lo;
-        drow[it] = m < a.M ? (partial ? (static_cast<long long>(split) * a.M + m) * a.Ng
-                                      : out_row(a, m))
-                           : -1;
-      }
-      float* base = partial ? a.ws : a.out;
+      const int nch = (ncols + 31) / 32;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        ptx::tmem_ld32(trow + c0, v);
-        if (c0 + 32 >= BN) {  // accumulator drained: release it to the MMA warp
+      for (int ci = 0; ci < nch; ++ci) {
+        const int c0 = ci * 32;
+        float cur[32];
+        ptx::tmem_ld32(trow + c0, cur);
+        if (ci + 1 >= nch) {  // accumulator drained: release it to the MMA warp
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty[acc]);
         }
-        if (c0 >= ncols) continue;
+        const uint32_t sbuf = sbuf0 + (nchunk & 1) * 4096;
+        if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
+        __syncwarp();
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
                            sbuf + lane * 128 + ((g ^ (lane & 7)) << 4)),
-                       "f"(v[4 * g]), "f"(v[4 * g + 1]), "f"(v[4 * g + 2]), "f"(v[4 * g + 3])
+                       "f"(cur[4 * g]), "f"(cur[4 * g + 1]), "f"(cur[4 * g + 2]), "f"(cur[4 * g + 3])
                        : "memory");
-        __syncwarp();
-        const int col = n0 + c0 + gg * 4;
-        const bool col_ok = c0 + gg * 4 < ncols;
-        float4 o[8];
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rr = it * 4 + rr_lo;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(o[it].x), "=f"(o[it].y), "=f"(o[it].z), "=f"(o[it].w)
-                       : "r"(sbuf + rr * 128 + ((gg ^ (rr & 7)) << 4)));
-        }
-        __syncwarp();
-        if (a.beta && !partial) {
-          float4 old[8];
-#pragma unroll
-          for (int it = 0; it < 8; ++it)
-            old[it] = (col_ok && drow[it] >= 0)
-                          ? *reinterpret_cast<const float4*>(base + drow[it] + col)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.tma_out) {
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (partial)
+              tma_store_3d(&tmC, sbuf, n0 + c0, m0, split);
+            else if (a.beta)
+              tma_reduce_add_2d(&tmC, sbuf, n0 + c0, m0);
+            else
+              tma_store_2d(&tmC, sbuf, n0 + c0, m0);
+            bulk_commit();
+          }
+        } else {
+          __syncwarp();
+          const int col = n0 + c0 + gg * 4;
+          const bool col_ok = c0 + gg * 4 < ncols;
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
-            o[it].x += old[it].x;
-            o[it].y += old[it].y;
-            o[it].z += old[it].z;
-            o[it].w += old[it].w;
+            const int rr = it * 4 + rr_lo;
+            const int m = m0 + rr;
+            float4 o;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w)
+                         : "r"(sbuf + rr * 128 + ((gg ^ (rr & 7)) << 4)));
+            if (col_ok && m < a.M) {
+              float* dst = partial ? a.ws + (static_cast<long long>(split) * a.M + m) * a.Ng + col
+                                   : a.out + out_row(a, m) + col;
+              float4* d4 = reinterpret_cast<float4*>(dst);
+              if (a.beta && !partial) {
+                const float4 old = *d4;
+                o.x += old.x;
+                o.y += old.y;
+                o.z += old.z;
+                o.w += old.w;
+              }
+              if (partial)
+                __stcg(d4, o);
+              else
+                *d4 = o;
+            }
           }
         }
-#pragma unroll
-        for (int it = 0; it < 8; ++it)
-          if (col_ok && drow[it] >= 0) {
-            if (partial)
-              __stcg(reinterpret_cast<float4*>(base + drow[it] + col), o[it]);
-            else
-              *reinterpret_cast<float4*>(base + drow[it] + col) = o[it];
-          }
+        ++nchunk;
       }
+      if (nch == 0) {  // tile entirely past Ng (cannot happen with tiles_n = ceil(Ng/BN))
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+      }
+      if (a.trace && threadIdx.x == 64 && j < 128) a.trace[blockIdx.x * 1024 + 513 + 2 * j] = clock64();
     }
+    if (lane == 0) bulk_wait_all();  // bulk stores complete before the CTA retires
   }
 
   ptx::tc_fence_before();
@@ -374,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem);
   }
+  if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 770] = gtimer();
 }
 
 // Deterministic split-K reduction: out[map(m)][n] (+)= sum_{s=0..S-1} ws[s][m][n],
@@ -382,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void __launch_bounds__(256) conv_splitk_reduce_kernel(const Prob a) {
   pdl_wait();
   pdl_trigger();
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 148) a.trace[blockIdx.x * 1024 + 771] = gtimer();
   const int ng4 = a.Ng >> 2;
   const long long total = static_cast<long long>(a.M) * ng4;
   const long long slice = static_cast<long long>(a.M) * a.Ng;
@@ -498,6 +560,7 @@ struct Workspace {
 };
 Workspace g_ws;
 size_t g_ws_default = 64ull << 20;
+long long* g_trace = nullptr;  // debug stamps, see accudnn_conv_trace
 
 // lazily owned workspace when the caller did not provide one
 size_t ws_capacity() {
@@ -541,8 +604,9 @@ int choose_splits(long long tiles, int kb_total, int bn, long long out_elems, in
 }
 
 template <int MODE, int BN, int STAGES>
-int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Prob& a, cudaStream_t st) {
-  constexpr size_t smem = STAGES * (kBM + BN) * kBK * 4 + 1024 + 1024 + 4 * 4096;
+int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
+             cudaStream_t st) {
+  constexpr size_t smem = STAGES * (kBM + BN) * kBK * 4 + 1024 + 1024 + 4 * 8192;
   static bool configured = false;
   if (!configured) {
     const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES>,
@@ -552,7 +616,8 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Prob& a, cudaSt
     configured = true;
   }
   const int grid = static_cast<int>(std::min<long long>(a.units, sm_count()));
-  cudaError_t e = launch_pdl(conv_sm100_kernel<MODE, BN, STAGES>, grid, kThreads, smem, st, ta, tb, a);
+  cudaError_t e =
+      launch_pdl(conv_sm100_kernel<MODE, BN, STAGES>, grid, kThreads, smem, st, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
   const long long vec = static_cast<long long>(a.M) * (a.Ng / 4);
@@ -674,11 +739,11 @@ bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb) {
 }
 
 template <int MODE>
-int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const Prob& a, int bn,
-                cudaStream_t st) {
-  if (bn == 256) return launch_t<MODE, 256, 4>(ta, tb, a, st);
-  if (bn == 128) return launch_t<MODE, 128, 6>(ta, tb, a, st);
-  return launch_t<MODE, 64, 8>(ta, tb, a, st);
+int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
+                int bn, cudaStream_t st) {
+  if (bn == 256) return launch_t<MODE, 256, 4>(ta, tb, tc, a, st);
+  if (bn == 128) return launch_t<MODE, 128, 6>(ta, tb, tc, a, st);
+  return launch_t<MODE, 64, 8>(ta, tb, tc, a, st);
 }
 
 // -1: could not encode the tensor maps (not launched)
@@ -692,9 +757,29 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
   a.units = a.tiles_m * a.tiles_n * a.splits;
   a.ws = g_ws.ws;
-  if (c.mode == FWD) return dispatch_bn<FWD>(ta, tb, a, cfg.bn, st);
-  if (c.mode == DGRAD) return dispatch_bn<DGRAD>(ta, tb, a, cfg.bn, st);
-  return dispatch_bn<WGRAD>(ta, tb, a, cfg.bn, st);
+  a.trace = g_trace;
+  // output tensor map for the bulk-store epilogue: the split-K workspace
+  // {Ng, M, S} (rows past M clip inside their own slice) or the row-major
+  // output {Ng, M}; scatter outputs (strided dgrad classes) store directly
+  CUtensorMap tc;
+  std::memset(&tc, 0, sizeof(tc));
+  a.tma_out = 0;
+  if (a.splits > 1) {
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.Ng), static_cast<cuuint64_t>(a.M),
+                                static_cast<cuuint64_t>(a.splits)};
+    const cuuint64_t str[2] = {static_cast<cuuint64_t>(a.Ng) * 4,
+                               static_cast<cuuint64_t>(a.Ng) * a.M * 4};
+    const cuuint32_t box[3] = {32, 32, 1};
+    a.tma_out = tiled_map(&tc, a.ws, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
+  } else if (!a.scatter) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.Ng), static_cast<cuuint64_t>(a.M)};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(a.Ng) * 4};
+    const cuuint32_t box[2] = {32, 32};
+    a.tma_out = tiled_map(&tc, a.out, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
+  }
+  if (c.mode == FWD) return dispatch_bn<FWD>(ta, tb, tc, a, cfg.bn, st);
+  if (c.mode == DGRAD) return dispatch_bn<DGRAD>(ta, tb, tc, a, cfg.bn, st);
+  return dispatch_bn<WGRAD>(ta, tb, tc, a, cfg.bn, st);
 }
 
 bool splits_ok(const Call& c, int s) {
@@ -936,6 +1021,14 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
   g_ws.bytes = ptr ? static_cast<size_t>(bytes) : 0;
   g_ws.owned = false;
   if (!ptr) g_ws_default = static_cast<size_t>(bytes);
+  return 0;
+}
+
+// debug: subsequent TMA-conv launches record clock64 stamps into buf
+// (1024 int64 per CTA: [0,256) producer issue of k-block i, [256,512) MMA
+// start of k-block i, [512,768) epilogue start/end of unit j); NULL = off
+extern "C" int accudnn_conv_trace(void* buf) {
+  accudnn::g_trace = static_cast<long long*>(buf);
   return 0;
 }
 
