@@ -7,6 +7,7 @@
 // atomics across blocks (the batch-norm sums run over up to k*112*112 rows,
 // so the cross-block accumulation is kept in double to avoid cancellation
 // in E[x^2] - E[x]^2).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,7 +52,6 @@ constexpr int kBnThreads = 512;
 constexpr int kBnGroup = 128;        // channels per channel group
 constexpr int kBnMaxBlocks = 1024;   // gx * Y
 constexpr int kBnMaxGroups = 64;     // C <= 8192
-constexpr int kBnMaxY = 128;         // row splits (bounds phase 2's slot sums)
 constexpr int kBnCounters = 64;
 
 struct BnWs {
@@ -105,11 +105,12 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
   __syncthreads();
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kBnThreads) bn_fused_kernel(const BnArgs a) {
+template <int MODE, bool CLUSTER>
+__global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[2][kBnThreads][4];
+  __shared__ __align__(16) float cpart[2][kBnGroup];  // CLUSTER: this block's partial
   __shared__ double dsum[kBnThreads];
   __shared__ float coef[6][kBnGroup];
   const int lanes = a.lanes;
@@ -182,38 +183,64 @@ __global__ void __launch_bounds__(kBnThreads) bn_fused_kernel(const BnArgs a) {
   }
   __syncthreads();
   const int gx = gridDim.x;
-  if (lane_r == 0) {  // row lanes summed in order
-    float t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
-    for (int rr = 0; rr < rows_per_pass; ++rr) {
-      const int src = rr * lanes + lane_c;
+  // fixed-shape tree over the row lanes
+  for (int n = rows_per_pass; n > 1;) {
+    const int half = (n + 1) / 2;
+    if (lane_r < n - half) {
+      const int src = (lane_r + half) * lanes + lane_c;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        t0[j] += red[0][src][j];
-        t1[j] += red[1][src][j];
+        red[0][threadIdx.x][j] += red[0][src][j];
+        red[1][threadIdx.x][j] += red[1][src][j];
       }
     }
-    float* slot = a.w.part + static_cast<size_t>(blockIdx.y * gx + blockIdx.x) * 2 * kBnGroup;
-    *reinterpret_cast<float4*>(slot + lane_c * 4) = make_float4(t0[0], t0[1], t0[2], t0[3]);
-    *reinterpret_cast<float4*>(slot + kBnGroup + lane_c * 4) = make_float4(t1[0], t1[1], t1[2], t1[3]);
+    n = half;
+    __syncthreads();
+  }
+  if (lane_r == 0) {
+    float* slot = CLUSTER ? &cpart[0][0]
+                          : a.w.part + static_cast<size_t>(blockIdx.y * gx + blockIdx.x) * 2 * kBnGroup;
+    *reinterpret_cast<float4*>(slot + lane_c * 4) =
+        make_float4(red[0][lane_c][0], red[0][lane_c][1], red[0][lane_c][2], red[0][lane_c][3]);
+    *reinterpret_cast<float4*>(slot + kBnGroup + lane_c * 4) =
+        make_float4(red[1][lane_c][0], red[1][lane_c][1], red[1][lane_c][2], red[1][lane_c][3]);
   }
 
-  grid_barrier(a.w.counters, gridDim.x * gridDim.y);
-
-  // ---- phase 2: the group's Y slots, chunked over threads, fixed order ----
   const int ch = lanes * 4;  // channels of this group
   const int V = 2 * ch;      // values: sum1 of ch channels, then sum2
-  const int T = kBnThreads / V;
-  {
+  int T = 1;
+  if constexpr (CLUSTER) {
+    // ---- cluster of the group's Y row splits: partials through DSMEM ----
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (threadIdx.x < V) {
+      const int v = threadIdx.x;
+      const int off = v < ch ? v : kBnGroup + (v - ch);
+      double t = 0.0;
+      for (unsigned r = 0; r < cluster.num_blocks(); ++r)  // rank order
+        t += static_cast<double>(cluster.map_shared_rank(&cpart[0][0], r)[off]);
+      dsum[v] = t;
+    }
+    cluster.sync();  // peers' partials are read before any block may exit
+  } else {
+    grid_barrier(a.w.counters, gridDim.x * gridDim.y);
+    // ---- phase 2: the group's Y slots, chunked over threads, fixed order ----
+    T = kBnThreads / V;
     const int v = threadIdx.x % V;
     const int chunk = threadIdx.x / V;
     double t = 0.0;
     if (chunk < T) {
-      const int y0 = chunk * a.Y / T, y1 = (chunk + 1) * a.Y / T;
+      const int y0 = chunk * a.Y / T, y1 = (chunk + 1) * a.Y / T;  // <= 16 slots (bn_launch)
       const int off = v < ch ? v : kBnGroup + (v - ch);
-#pragma unroll 4
-      for (int yy = y0; yy < y1; ++yy)
-        t += static_cast<double>(
-            __ldcg(a.w.part + static_cast<size_t>(yy * gx + blockIdx.x) * 2 * kBnGroup + off));
+      float pv[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        pv[k] = (y0 + k < y1)
+                    ? __ldcg(a.w.part + static_cast<size_t>((y0 + k) * gx + blockIdx.x) * 2 * kBnGroup + off)
+                    : 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) t += static_cast<double>(pv[k]);
     }
     dsum[threadIdx.x] = t;
   }
@@ -333,44 +360,67 @@ __global__ void __launch_bounds__(kBnThreads) bn_fused_kernel(const BnArgs a) {
   }
 }
 
-// cooperative grid: channel groups of lanes*4 <= 128 channels x Y row splits,
-// all blocks co-resident (the occupancy limit), ~2 blocks per SM, >= 16 rows
-// per block, Y <= kBnMaxY
+// Launch shapes (32-channel groups, gx = C/32, 512 threads):
+//  * cluster: the Y <= 16 row splits of a group form one thread-block
+//    cluster and exchange partials through distributed shared memory -- no
+//    global synchronisation; used for narrow layers with few rows;
+//  * cooperative: Y row splits over the whole grid (all CTAs co-resident,
+//    2 per SM), partials in the workspace, one grid barrier; for the large
+//    early-stage layers that need every SM streaming.
 template <int MODE>
 int bn_launch(BnArgs a, cudaStream_t st) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<MODE>, kBnThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<MODE, false>, kBnThreads, 0);
     if (occ < 1) occ = 1;
+    cudaFuncSetAttribute(bn_fused_kernel<MODE, true>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);
   int l = a.C / 4;
-  if (l > kBnGroup / 4) l = kBnGroup / 4;
+  if (l > 8) l = 8;
   if (l < 1) l = 1;
   a.lanes = l;
   const int gx = (a.C / 4 + l - 1) / l;
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kBnThreads);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  // measured (tools/bn_bench.py, k* = 27 shapes): clusters win for narrow
+  // layers with few rows, the cooperative grid for wide or tall ones
+  const bool cluster = a.C <= 256 && a.M <= 16LL * 2048;
+  if (cluster) {
+    long long y = std::max<long long>(1, (2LL * sms + gx - 1) / gx);
+    y = std::min<long long>(y, (a.M + 31) / 32);
+    y = std::min<long long>(y, 16);
+    if (y < 1) y = 1;
+    a.Y = static_cast<int>(y);
+    cfg.gridDim = dim3(gx, a.Y);
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = a.Y;
+    attr[0].val.clusterDim.z = 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE, true>, a));
+  }
+  const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);
   if (gx > max_blocks) return static_cast<int>(cudaErrorInvalidConfiguration);
-  long long y = (2LL * sms + gx - 1) / gx;
+  const int T = kBnThreads / (2 * 4 * l);
+  long long y = (max_blocks + gx - 1) / gx;
   y = std::min<long long>(y, (a.M + 15) / 16);
-  y = std::min<long long>(y, kBnMaxY);
+  y = std::min<long long>(y, 16LL * T);
   y = std::min<long long>(y, max_blocks / gx);
   if (y < 1) y = 1;
   a.Y = static_cast<int>(y);
-  cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(gx, a.Y);
-  cfg.blockDim = dim3(kBnThreads);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE>, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE, false>, a));
 }
 
 // ---------------------------------------------------------------------------

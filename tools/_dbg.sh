@@ -1,6 +1,2 @@
-timeout 900 python -m pytest tests/test_conv_gpu.py -q -x > gpurun_out/pytest_conv.log 2>&1
-python tools/conv_trace.py fwd 27 1024 14 14 256 1 1 0 > gpurun_out/trace1.log 2>&1
-python tools/conv_trace.py fwd 27 64 56 56 256 1 1 0 > gpurun_out/trace3.log 2>&1
-timeout 600 python tools/conv_bench.py 27 gpurun_out/conv_bench.json > gpurun_out/conv_bench.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
-timeout 300 python bench.py > gpurun_out/bench.log 2>&1
+timeout 600 ncu --set full --import-source on -k regex:bn_fused -s 2 -c 1 -o gpurun_out/prof_bn1 python tools/_bn_one.py 1323 512 > gpurun_out/ncu_bn1.log 2>&1
+timeout 600 ncu --set full --import-source on -k regex:bn_fused -s 2 -c 1 -o gpurun_out/prof_bn2 python tools/_bn_one.py 5292 256 > gpurun_out/ncu_bn2.log 2>&1
