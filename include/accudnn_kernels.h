@@ -73,6 +73,19 @@ int accudnn_bn_bwd(const float* x, const float* dy, long long M, int C,
                    const float* save_invstd, int relu, float* dx, int dx_beta,
                    float* dgamma, float* dbeta, void* ws, void* stream);
 
+/* the residual tail of a ResNet block as one op: y = relu(bn(x) + skip)
+ * (training-mode BN over [M][C]); backward recomputes the mask from the
+ * inputs and writes both gradients (dx: BN backward, dskip: masked dy;
+ * each accumulates when its beta flag is 1). */
+int accudnn_bn_add_relu_fwd(const float* x, const float* skip, long long M, int C,
+                            const float* gamma, const float* beta, float eps, float* y,
+                            float* save_mean, float* save_invstd, float* running_mean,
+                            float* running_var, float momentum, void* ws, void* stream);
+int accudnn_bn_add_relu_bwd(const float* x, const float* skip, const float* dy, long long M,
+                            int C, const float* gamma, const float* beta,
+                            const float* save_mean, const float* save_invstd, float* dx,
+                            int dx_beta, float* dskip, int dskip_beta, float* dgamma,
+                            float* dbeta, void* ws, void* stream);
 int accudnn_relu_fwd(const float* x, float* y, long long n, void* stream);
 /* dx (+)= dy * (x > 0) */
 int accudnn_relu_bwd(const float* x, const float* dy, float* dx, long long n,

@@ -78,7 +78,7 @@ class TorchResNet:
             x = x_img if op["in0"] == -2 else t[op["in0"]]
             if kind == "conv":
                 y = self._conv(x, self._w(p, op), op["stride"], op["pad"])
-            elif kind in ("bn", "bn_relu"):
+            elif kind in ("bn", "bn_relu", "bn_add_relu"):
                 c = op["channels"]
                 so = op["stat_off"]
                 rm = stats[so + 2 * c:so + 3 * c]
@@ -88,6 +88,8 @@ class TorchResNet:
                                  momentum=0.1, eps=1e-5)
                 if kind == "bn_relu":
                     y = F.relu(y)
+                elif kind == "bn_add_relu":  # relu(bn(conv) + shortcut), one op
+                    y = F.relu(y + t[op["in1"]])
             elif kind == "relu":
                 y = F.relu(x)
             elif kind == "add":

@@ -84,6 +84,9 @@ struct BnArgs {
   float* dbeta;
   float* dx;             // mode 1: data gradient (+= when dx_beta)
   int dx_beta;
+  const float* skip;     // SKIP: y = relu(bn(x) + skip); backward mask uses it too
+  float* dskip;          // SKIP, mode 1: gradient of the shortcut (+= when dskip_beta)
+  int dskip_beta;
   BnWs w;
 };
 
@@ -105,8 +108,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
   __syncthreads();
 }
 
-template <int MODE, bool CLUSTER>
-__global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a) {
+template <int MODE, bool CLUSTER, bool SKIP>
+__global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel(const BnArgs a) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[2][kBnThreads][4];
@@ -137,8 +140,9 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
       be[j] = a.beta[c + j];
     }
   }
-  auto consume = [&](const float4 v, const float4 d) {
+  auto consume = [&](const float4 v, const float4 d, const float4 sk4) {
     const float xv[4] = {v.x, v.y, v.z, v.w};
+    const float sk[4] = {sk4.x, sk4.y, sk4.z, sk4.w};
     if (MODE == 0) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
       for (int j = 0; j < 4; ++j) {
         const float xh = (xv[j] - mu[j]) * is[j];
         float g = dv[j];
-        if (a.relu && (xh * ga[j] + be[j]) <= 0.f) g = 0.f;
+        if (a.relu && (xh * ga[j] + be[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
         a0[j] += g;
         a1[j] += g * xh;
       }
@@ -161,19 +165,24 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
   if (c_ok) {
     long long r = r_begin + lane_r;
     for (; r + 3 * step < r_end; r += 4 * step) {  // 4 rows in flight
-      float4 v[4], d[4];
+      float4 v[4], d[4], sk[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
         if (MODE == 1) d[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * C + c));
+        if (MODE == 1 && SKIP)
+          sk[u] = __ldg(reinterpret_cast<const float4*>(a.skip + (r + u * step) * C + c));
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) consume(v[u], MODE == 1 ? d[u] : v[u]);
+      for (int u = 0; u < 4; ++u)
+        consume(v[u], MODE == 1 ? d[u] : v[u], (MODE == 1 && SKIP) ? sk[u] : v[u]);
     }
     for (; r < r_end; r += step) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
       const float4 d = MODE == 1 ? __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)) : v;
-      consume(v, d);
+      const float4 sk =
+          (MODE == 1 && SKIP) ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v;
+      consume(v, d, sk);
     }
   }
 #pragma unroll
@@ -290,11 +299,17 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
   if (MODE == 0) {
     const float sc[4] = {coef[0][cl], coef[0][cl + 1], coef[0][cl + 2], coef[0][cl + 3]};
     const float sh[4] = {coef[1][cl], coef[1][cl + 1], coef[1][cl + 2], coef[1][cl + 3]};
-    auto f = [&](float4 v) {
+    auto f = [&](float4 v, const float4 k4) {
       v.x = v.x * sc[0] + sh[0];
       v.y = v.y * sc[1] + sh[1];
       v.z = v.z * sc[2] + sh[2];
       v.w = v.w * sc[3] + sh[3];
+      if (SKIP) {
+        v.x += k4.x;
+        v.y += k4.y;
+        v.z += k4.z;
+        v.w += k4.w;
+      }
       if (a.relu) {
         v.x = fmaxf(v.x, 0.f);
         v.y = fmaxf(v.y, 0.f);
@@ -305,14 +320,21 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
     };
     long long r = r_begin + lane_r;
     for (; r + 3 * step < r_end; r += 4 * step) {
-      float4 v[4];
+      float4 v[4], kv[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
+      for (int u = 0; u < 4; ++u) {
+        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
+        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r + u * step) * C + c)) : v[u];
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<float4*>(a.y + (r + u * step) * C + c) = f(v[u]);
+      for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<float4*>(a.y + (r + u * step) * C + c) = f(v[u], kv[u]);
     }
-    for (; r < r_end; r += step)
-      *reinterpret_cast<float4*>(a.y + r * C + c) = f(__ldg(reinterpret_cast<const float4*>(a.x + r * C + c)));
+    for (; r < r_end; r += step) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
+      *reinterpret_cast<float4*>(a.y + r * C + c) =
+          f(v, SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v);
+    }
   } else {
     float mg[4], mgx[4], k0[4];
 #pragma unroll
@@ -321,42 +343,51 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
       mgx[j] = coef[1][cl + j];
       k0[j] = ga[j] * is[j];
     }
-    auto f = [&](const float4 xv4, const float4 dv4, long long r) {
+    auto f = [&](const float4 xv4, const float4 dv4, const float4 k4, long long r) {
       const float xv[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
       const float dv[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
-      float o[4];
+      const float sk[4] = {k4.x, k4.y, k4.z, k4.w};
+      float o[4], gg[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float xh = (xv[j] - mu[j]) * is[j];
         float g = dv[j];
-        if (a.relu && (xh * ga[j] + be[j]) <= 0.f) g = 0.f;
+        if (a.relu && (xh * ga[j] + be[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
+        gg[j] = g;
         o[j] = k0[j] * (g - mg[j] - xh * mgx[j]);
       }
-      float4 out = make_float4(o[0], o[1], o[2], o[3]);
-      float4* d = reinterpret_cast<float4*>(a.dx + r * C + c);
-      if (a.dx_beta) {
-        const float4 old = *d;
-        out.x += old.x;
-        out.y += old.y;
-        out.z += old.z;
-        out.w += old.w;
-      }
-      *d = out;
+      auto put = [&](float* base, const float* val, int beta) {
+        float4 out = make_float4(val[0], val[1], val[2], val[3]);
+        float4* d = reinterpret_cast<float4*>(base + r * C + c);
+        if (beta) {
+          const float4 old = *d;
+          out.x += old.x;
+          out.y += old.y;
+          out.z += old.z;
+          out.w += old.w;
+        }
+        *d = out;
+      };
+      put(a.dx, o, a.dx_beta);
+      if (SKIP) put(a.dskip, gg, a.dskip_beta);  // d(shortcut) = masked dy
     };
     long long r = r_begin + lane_r;
     for (; r + 3 * step < r_end; r += 4 * step) {
-      float4 xv[4], dv[4];
+      float4 xv[4], dv[4], kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         xv[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
         dv[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * C + c));
+        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r + u * step) * C + c)) : xv[u];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], r + u * step);
+      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], kv[u], r + u * step);
     }
-    for (; r < r_end; r += step)
-      f(__ldg(reinterpret_cast<const float4*>(a.x + r * C + c)),
-        __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)), r);
+    for (; r < r_end; r += step) {
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
+      f(xv, __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)),
+        SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : xv, r);
+    }
   }
 }
 
@@ -367,13 +398,14 @@ __global__ void __launch_bounds__(kBnThreads, 2) bn_fused_kernel(const BnArgs a)
 //  * cooperative: Y row splits over the whole grid (all CTAs co-resident,
 //    2 per SM), partials in the workspace, one grid barrier; for the large
 //    early-stage layers that need every SM streaming.
-template <int MODE>
+template <int MODE, bool SKIP>
 int bn_launch(BnArgs a, cudaStream_t st) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<MODE, false>, kBnThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<MODE, false, SKIP>,
+                                                  kBnThreads, 0);
     if (occ < 1) occ = 1;
-    cudaFuncSetAttribute(bn_fused_kernel<MODE, true>,
+    cudaFuncSetAttribute(bn_fused_kernel<MODE, true, SKIP>,
                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   int sms = 0, dev = 0;
@@ -394,7 +426,8 @@ int bn_launch(BnArgs a, cudaStream_t st) {
   cfg.numAttrs = 2;
   // measured (tools/bn_bench.py, k* = 27 shapes): clusters win for narrow
   // layers with few rows, the cooperative grid for wide or tall ones
-  const bool cluster = a.C <= 256 && a.M <= 16LL * 2048;
+  const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);
+  const bool cluster = (a.C <= 256 && a.M <= 16LL * 2048) || gx > max_blocks;
   if (cluster) {
     long long y = std::max<long long>(1, (2LL * sms + gx - 1) / gx);
     y = std::min<long long>(y, (a.M + 31) / 32);
@@ -406,10 +439,8 @@ int bn_launch(BnArgs a, cudaStream_t st) {
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = a.Y;
     attr[0].val.clusterDim.z = 1;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE, true>, a));
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE, true, SKIP>, a));
   }
-  const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);
-  if (gx > max_blocks) return static_cast<int>(cudaErrorInvalidConfiguration);
   const int T = kBnThreads / (2 * 4 * l);
   long long y = (max_blocks + gx - 1) / gx;
   y = std::min<long long>(y, (a.M + 15) / 16);
@@ -420,7 +451,7 @@ int bn_launch(BnArgs a, cudaStream_t st) {
   cfg.gridDim = dim3(gx, a.Y);
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE, false>, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, bn_fused_kernel<MODE, false, SKIP>, a));
 }
 
 // ---------------------------------------------------------------------------
@@ -854,7 +885,7 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
   a.run_var = running_var;
   a.y = y;
   a.w = bn_ws(ws, C);
-  return bn_launch<0>(a, S(stream));
+  return bn_launch<0, false>(a, S(stream));
 }
 
 extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int C,
@@ -877,7 +908,62 @@ extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int 
   a.dx = dx;
   a.dx_beta = dx_beta;
   a.w = bn_ws(ws, C);
-  return bn_launch<1>(a, S(stream));
+  return bn_launch<1, false>(a, S(stream));
+}
+
+// y = relu(bn(x) + skip) over [M][C] (the residual tail of a ResNet block)
+extern "C" int accudnn_bn_add_relu_fwd(const float* x, const float* skip, long long M, int C,
+                                       const float* gamma, const float* beta, float eps, float* y,
+                                       float* save_mean, float* save_invstd, float* running_mean,
+                                       float* running_var, float momentum, void* ws,
+                                       void* stream) {
+  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
+  BnArgs a{};
+  a.x = x;
+  a.skip = skip;
+  a.M = M;
+  a.C = C;
+  a.relu = 1;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.eps = eps;
+  a.momentum = momentum;
+  a.save_mean = save_mean;
+  a.save_invstd = save_invstd;
+  a.run_mean = running_mean;
+  a.run_var = running_var;
+  a.y = y;
+  a.w = bn_ws(ws, C);
+  return bn_launch<0, true>(a, S(stream));
+}
+
+// backward of y = relu(bn(x) + skip): g = dy * [bn(x) + skip > 0] (mask
+// recomputed from the inputs), dskip (+)= g, dx (+)= BN backward of g
+extern "C" int accudnn_bn_add_relu_bwd(const float* x, const float* skip, const float* dy,
+                                       long long M, int C, const float* gamma, const float* beta,
+                                       const float* save_mean, const float* save_invstd,
+                                       float* dx, int dx_beta, float* dskip, int dskip_beta,
+                                       float* dgamma, float* dbeta, void* ws, void* stream) {
+  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
+  BnArgs a{};
+  a.x = x;
+  a.skip = skip;
+  a.dy = dy;
+  a.M = M;
+  a.C = C;
+  a.relu = 1;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.mean = save_mean;
+  a.invstd = save_invstd;
+  a.dgamma = dgamma;
+  a.dbeta = dbeta;
+  a.dx = dx;
+  a.dx_beta = dx_beta;
+  a.dskip = dskip;
+  a.dskip_beta = dskip_beta;
+  a.w = bn_ws(ws, C);
+  return bn_launch<1, true>(a, S(stream));
 }
 
 extern "C" int accudnn_relu_fwd(const float* x, float* y, long long n, void* stream) {

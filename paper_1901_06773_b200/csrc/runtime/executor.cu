@@ -319,6 +319,16 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
             "bn fwd");
         break;
       }
+      case OpKind::bn_add_relu: {
+        const int C = op.channels;
+        float* sp = I.stats + op.stat_off;
+        ckl(accudnn_bn_add_relu_fwd(act(op.in0, s), act(op.in1, s), elems(o) / C, C,
+                                    I.params + op.g_off, I.params + op.beta_off, cfg_.bn_eps, y,
+                                    sp, sp + C, sp + 2 * C, sp + 3 * C, cfg_.bn_momentum, I.bn_ws,
+                                    csv),
+            "bn_add_relu fwd");
+        break;
+      }
       case OpKind::relu:
         ckl(accudnn_relu_fwd(act(op.in0, s), y, elems(o), csv), "relu fwd");
         break;
@@ -367,6 +377,17 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
                            grad(op.in0), beta_for(op.in0, o), I.grads + op.g_off,
                            I.grads + op.beta_off, I.bn_ws, csv),
             "bn bwd");
+        break;
+      }
+      case OpKind::bn_add_relu: {
+        const int C = op.channels;
+        float* sp = I.stats + op.stat_off;
+        ckl(accudnn_bn_add_relu_bwd(act(op.in0, s), act(op.in1, s), grad(o), elems(o) / C, C,
+                                    I.params + op.g_off, I.params + op.beta_off, sp, sp + C,
+                                    grad(op.in0), beta_for(op.in0, o), grad(op.in1),
+                                    beta_for(op.in1, o), I.grads + op.g_off,
+                                    I.grads + op.beta_off, I.bn_ws, csv),
+            "bn_add_relu bwd");
         break;
       }
       case OpKind::relu:

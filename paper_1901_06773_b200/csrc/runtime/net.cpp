@@ -26,6 +26,7 @@ const char* op_kind_name(OpKind k) {
     case OpKind::avgpool: return "avgpool";
     case OpKind::fc: return "fc";
     case OpKind::xent: return "xent";
+    case OpKind::bn_add_relu: return "bn_add_relu";
   }
   return "?";
 }
@@ -55,6 +56,15 @@ class Builder {
     op.kind = relu ? OpKind::bn_relu : OpKind::bn;
     op.name = name;
     op.in0 = in;
+    op.channels = in_shape(in).c;
+    return push(op, in_shape(in));
+  }
+  int bn_add_relu(const std::string& name, int in, int skip) {
+    Op op;
+    op.kind = OpKind::bn_add_relu;
+    op.name = name;
+    op.in0 = in;
+    op.in1 = skip;
     op.channels = in_shape(in).c;
     return push(op, in_shape(in));
   }
@@ -140,14 +150,12 @@ void imagenet_bottleneck(Net& net, const int (&blocks)[4]) {
       y = b.conv(p + "conv2", y, width, 3, stride, 1);
       y = b.bn(p + "bn2", y, true);
       y = b.conv(p + "conv3", y, width * 4, 1, 1, 0);
-      y = b.bn(p + "bn3", y, false);
       int sc = in;
       if (i == 0) {
         sc = b.conv(p + "downsample.conv", in, width * 4, 1, stride, 0);
         sc = b.bn(p + "downsample.bn", sc, false);
       }
-      y = b.add(p + "add", y, sc);
-      x = b.relu(p + "relu", y);
+      x = b.bn_add_relu(p + "bn3", y, sc);  // relu(bn3(conv3) + shortcut)
       cin = width * 4;
     }
   }
@@ -173,14 +181,12 @@ void imagenet_basic(Net& net, const int (&blocks)[4]) {
       int y = b.conv(p + "conv1", in, width, 3, stride, 1);
       y = b.bn(p + "bn1", y, true);
       y = b.conv(p + "conv2", y, width, 3, 1, 1);
-      y = b.bn(p + "bn2", y, false);
       int sc = in;
       if (stride != 1 || cin != width) {
         sc = b.conv(p + "downsample.conv", in, width, 1, stride, 0);
         sc = b.bn(p + "downsample.bn", sc, false);
       }
-      y = b.add(p + "add", y, sc);
-      x = b.relu(p + "relu", y);
+      x = b.bn_add_relu(p + "bn2", y, sc);  // relu(bn2(conv2) + shortcut)
       cin = width;
     }
   }
@@ -204,14 +210,12 @@ void cifar_basic(Net& net, int n) {
       int y = b.conv(p + "conv1", in, width, 3, stride, 1);
       y = b.bn(p + "bn1", y, true);
       y = b.conv(p + "conv2", y, width, 3, 1, 1);
-      y = b.bn(p + "bn2", y, false);
       int sc = in;
       if (stride != 1 || cin != width) {
         sc = b.conv(p + "shortcut.conv", in, width, 1, stride, 0);
         sc = b.bn(p + "shortcut.bn", sc, false);
       }
-      y = b.add(p + "add", y, sc);
-      x = b.relu(p + "relu", y);
+      x = b.bn_add_relu(p + "bn2", y, sc);  // relu(bn2(conv2) + shortcut)
       cin = width;
     }
   }
@@ -273,7 +277,7 @@ void finalize(Net& net) {
       off = align4(off + static_cast<long long>(op.cout) * op.cin);
       op.b_off = off;
       off = align4(off + op.cout);
-    } else if (op.kind == OpKind::bn || op.kind == OpKind::bn_relu) {
+    } else if (is_bn(op.kind)) {
       op.g_off = off;
       off = align4(off + op.channels);
       op.beta_off = off;
@@ -328,6 +332,7 @@ bool bwd_reads_input(const Op& op) {
     case OpKind::fc:
     case OpKind::bn:
     case OpKind::bn_relu:
+    case OpKind::bn_add_relu:  // reads both inputs (BN input + the shortcut, for the mask)
     case OpKind::relu:
     case OpKind::maxpool:
     case OpKind::xent:
@@ -586,6 +591,11 @@ OpCost op_cost(const Net& net, int i) {
       break;
     case OpKind::bn: c.fwd = 8 * out; c.bwd = 12 * out; c.params = 2LL * op.channels; break;
     case OpKind::bn_relu: c.fwd = 9 * out; c.bwd = 13 * out; c.params = 2LL * op.channels; break;
+    case OpKind::bn_add_relu:
+      c.fwd = 10 * out;
+      c.bwd = 14 * out;
+      c.params = 2LL * op.channels;
+      break;
     case OpKind::relu: c.fwd = out; c.bwd = out; break;
     case OpKind::add: c.fwd = out; c.bwd = out; break;
     case OpKind::maxpool: c.fwd = out * op.pk * op.pk; c.bwd = 2 * c.fwd; break;
@@ -613,6 +623,7 @@ const char* layer_type_of(OpKind k, const char** tag) {
     case OpKind::avgpool: return "pooling";
     case OpKind::add: *tag = "eltwise"; return "other";
     case OpKind::xent: *tag = "loss"; return "other";
+    case OpKind::bn_add_relu: *tag = "bn_add_relu"; return "other";
   }
   return "other";
 }
@@ -695,7 +706,7 @@ std::string describe_net_json(const Net& net) {
       o["w_off"] = op.w_off;
       if (op.b_off >= 0) o["b_off"] = op.b_off;
     }
-    if (op.kind == OpKind::bn || op.kind == OpKind::bn_relu) {
+    if (is_bn(op.kind)) {
       o["channels"] = op.channels;
       o["g_off"] = op.g_off;
       o["beta_off"] = op.beta_off;

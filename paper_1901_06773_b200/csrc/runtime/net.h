@@ -24,7 +24,13 @@
 
 namespace accudnn {
 
-enum class OpKind : int { conv, bn, bn_relu, relu, add, maxpool, avgpool, fc, xent };
+// bn_add_relu: y = relu(bn(in0) + in1), the residual tail of a ResNet block
+// as one op (its only output is the block output; bn(in0) and the sum are
+// never materialised)
+enum class OpKind : int { conv, bn, bn_relu, relu, add, maxpool, avgpool, fc, xent, bn_add_relu };
+inline bool is_bn(OpKind k) {
+  return k == OpKind::bn || k == OpKind::bn_relu || k == OpKind::bn_add_relu;
+}
 const char* op_kind_name(OpKind k);
 
 constexpr int kImage = -2;  // "input" id of the network input batch

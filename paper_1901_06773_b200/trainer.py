@@ -96,7 +96,7 @@ def init_params(describe, seed=0):
             bound = 1.0 / cin ** 0.5
             p[op["w_off"]:op["w_off"] + cout * cin] = rng.uniform(-bound, bound, cout * cin)
             p[op["b_off"]:op["b_off"] + cout] = rng.uniform(-bound, bound, cout)
-        elif op["kind"] in ("bn", "bn_relu"):
+        elif op["kind"] in ("bn", "bn_relu", "bn_add_relu"):
             c = op["channels"]
             p[op["g_off"]:op["g_off"] + c] = 1.0
             p[op["beta_off"]:op["beta_off"] + c] = 0.0

@@ -85,6 +85,44 @@ def test_batchnorm_fwd_bwd(cuda_dev, M, C, relu):
     assert torch.equal(y2, y_d) and torch.equal(mean2, mean_d)
 
 
+@pytest.mark.parametrize("M,C", [(42 * 56 * 56, 256), (27 * 14 * 14, 1024), (27 * 7 * 7, 2048),
+                                 (8 * 32 * 32, 16), (5, 8)])
+def test_bn_add_relu(cuda_dev, M, C):
+    """y = relu(bn(x) + skip) as one op, forward and backward (both input
+    gradients, accumulate flags) vs torch fp32 autograd of the unfused ops."""
+    lib = _native.cuda_lib()
+    g = torch.Generator().manual_seed(M + 7 * C)
+    x = torch.randn(M, C, generator=g) * 1.5 - 0.3
+    skip = torch.randn(M, C, generator=g)
+    gamma = torch.rand(C, generator=g) + 0.5
+    beta = torch.randn(C, generator=g) * 0.1
+    dy = torch.randn(M, C, generator=g)
+    xr, sr = x.clone().requires_grad_(True), skip.clone().requires_grad_(True)
+    gr, br = gamma.clone().requires_grad_(True), beta.clone().requires_grad_(True)
+    y_ref = F.relu(F.batch_norm(xr, None, None, gr, br, training=True, eps=1e-5) + sr)
+    y_ref.backward(dy)
+    d = cuda_dev
+    x_d, s_d, dy_d, g_d, b_d = x.to(d), skip.to(d), dy.to(d), gamma.to(d), beta.to(d)
+    y_d = torch.empty_like(x_d)
+    mean_d, inv_d = torch.empty(C, device=d), torch.empty(C, device=d)
+    ws = torch.zeros(lib.accudnn_bn_workspace_bytes(C) // 4 + 1, device=d)
+    assert lib.accudnn_bn_add_relu_fwd(ptr(x_d), ptr(s_d), M, C, ptr(g_d), ptr(b_d), 1e-5, ptr(y_d),
+                                       ptr(mean_d), ptr(inv_d), None, None, 0.1, ptr(ws), None) == 0
+    dx_d = torch.full_like(x_d, float("nan"))
+    base = torch.randn_like(x_d)
+    ds_d = base.clone()  # the shortcut gradient accumulates (beta = 1)
+    dg_d, db_d = torch.empty(C, device=d), torch.empty(C, device=d)
+    assert lib.accudnn_bn_add_relu_bwd(ptr(x_d), ptr(s_d), ptr(dy_d), M, C, ptr(g_d), ptr(b_d),
+                                       ptr(mean_d), ptr(inv_d), ptr(dx_d), 0, ptr(ds_d), 1,
+                                       ptr(dg_d), ptr(db_d), ptr(ws), None) == 0
+    torch.cuda.synchronize()
+    assert rel(y_d, y_ref.detach()) < 1e-5
+    assert rel(dx_d, xr.grad) < 1e-4
+    assert rel(ds_d - base, sr.grad) < 1e-5
+    assert rel(dg_d, gr.grad) < 1e-4
+    assert rel(db_d, br.grad) < 1e-5
+
+
 def test_batchnorm_shared_workspace_mixed_widths(cuda_dev):
     """one workspace serves layers of different channel counts in turn (as in
     the executor): every call must still finalise its own statistics."""

@@ -45,7 +45,7 @@ def flat_from_torchvision(model, desc):
             w = sd["fc.weight"].numpy()
             p[op["w_off"]:op["w_off"] + w.size] = w.ravel()
             p[op["b_off"]:op["b_off"] + op["cout"]] = sd["fc.bias"].numpy()
-        elif op["kind"] in ("bn", "bn_relu"):
+        elif op["kind"] in ("bn", "bn_relu", "bn_add_relu"):
             c = op["channels"]
             p[op["g_off"]:op["g_off"] + c] = sd[tvname + ".weight"].numpy()
             p[op["beta_off"]:op["beta_off"] + c] = sd[tvname + ".bias"].numpy()
