@@ -75,6 +75,8 @@ struct Prob {
   float* ws;           // split-K partials [split][M][Ng]
   long long* trace;    // debug: per-CTA clock64 stamps (accudnn_conv_trace), or nullptr
   int tma_out;         // epilogue stores through tmC (bulk tensor stores / reduce-adds)
+  int a_packed;        // WGRAD: A stage (4 MN atoms) is one 3-D TMA box
+  int b_packed;        // DGRAD: B stage (BN/32 MN atoms) is one 4-D box; WGRAD 1x1: one 3-D box
 };
 
 // ---- TMA PTX -------------------------------------------------------------------
@@ -92,6 +94,15 @@ __device__ __forceinline__ void tma_3d(const CUtensorMap* tm, uint32_t dst, uint
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(const CUtensorMap* tm, uint32_t dst, uint64_t* bar, int c0,
+                                       int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void tma_im2col(const CUtensorMap* tm, uint32_t dst, uint64_t* bar,
@@ -273,20 +284,32 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_im2col(&tmA, sA, bar, co0, pj + a.lo_w, pi + a.lo_h, pn,
                          static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
             }
+            if (a.b_packed) {  // {ci 32, co, ci-block, tap}: all BN/32 atoms at once
+              tma_4d(&tmB, sB, bar, 0, co0, n0 / 32, tap);
+            } else {
 #pragma unroll
-            for (int b = 0; b < BN / 32; ++b)
-              tma_3d(&tmB, sB + b * 4096, bar, n0 + 32 * b, tap, co0);
+              for (int b = 0; b < BN / 32; ++b)
+                tma_3d(&tmB, sB + b * 4096, bar, n0 + 32 * b, tap, co0);
+            }
           } else {
+            if (a.a_packed) {  // {co 32, pixel, co-block}: the 4 atoms of the stage at once
+              tma_3d(&tmA, sA, bar, 0, kk, m0 / 32);
+            } else {
 #pragma unroll
-            for (int b = 0; b < kBM / 32; ++b) tma_2d(&tmA, sA + b * 4096, bar, m0 + 32 * b, kk);
-            const int pq = a.P * a.Q;
-            const int n = kk / pq, rem = kk - n * pq;
-            const int p = rem / a.Q, q = rem - p * a.Q;
+              for (int b = 0; b < kBM / 32; ++b) tma_2d(&tmA, sA + b * 4096, bar, m0 + 32 * b, kk);
+            }
+            if (a.b_packed) {  // 1x1 stride 1: {ci 32, pixel, ci-block}
+              tma_3d(&tmB, sB, bar, 0, kk, n0 / 32);
+            } else {
+              const int pq = a.P * a.Q;
+              const int n = kk / pq, rem = kk - n * pq;
+              const int p = rem / a.Q, q = rem - p * a.Q;
 #pragma unroll
-            for (int b = 0; b < BN / 32; ++b)
-              tma_im2col(&tmB, sB + b * 4096, bar, wt_c + 32 * b, q * a.stride - a.pad,
-                         p * a.stride - a.pad, n, static_cast<uint16_t>(wt_s),
-                         static_cast<uint16_t>(wt_r));
+              for (int b = 0; b < BN / 32; ++b)
+                tma_im2col(&tmB, sB + b * 4096, bar, wt_c + 32 * b, q * a.stride - a.pad,
+                           p * a.stride - a.pad, n, static_cast<uint16_t>(wt_s),
+                           static_cast<uint16_t>(wt_r));
+            }
           }
         }
       }
@@ -689,8 +712,7 @@ bool bn_ok(const Call& c, int bn) {
   }
 }
 
-bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb) {
-  const Prob& a = c.a;
+bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb, Prob& a) {
   if (c.mode == FWD) {
     bool ok;
     if (a.a_tiled) {
@@ -721,21 +743,59 @@ bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb) {
       ok = im2col_map(ta, c.A, a.N, a.P, a.Q, a.K, a.lo_h, a.lo_w, a.Hc - a.P + a.lo_h,
                       a.Wc - a.Q + a.lo_w, 1, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
     }
+    if (!ok) return false;
+    // B: all BN/32 MN atoms (32 ci x 32 co) of a stage as one 4-D box over
+    // w viewed as {ci 32, co, ci-block, tap}; else one 3-D box per atom
+    a.b_packed = 0;
+    if (a.C % 32 == 0 && a.C >= bn) {
+      const cuuint64_t pd[4] = {32, static_cast<cuuint64_t>(a.K), static_cast<cuuint64_t>(a.C / 32),
+                                static_cast<cuuint64_t>(a.R) * a.S};
+      const cuuint64_t ps[3] = {static_cast<cuuint64_t>(a.C) * a.R * a.S * 4, 128,
+                                static_cast<cuuint64_t>(a.C) * 4};
+      const cuuint32_t pbox[4] = {32, 32, static_cast<cuuint32_t>(bn / 32), 1};
+      if (tiled_map(tb, c.B, 4, pd, ps, pbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+        a.b_packed = 1;
+        return true;
+      }
+    }
     const cuuint64_t bd[3] = {static_cast<cuuint64_t>(a.C), static_cast<cuuint64_t>(a.R) * a.S,
                               static_cast<cuuint64_t>(a.K)};
     const cuuint64_t bs[2] = {static_cast<cuuint64_t>(a.C) * 4,
                               static_cast<cuuint64_t>(a.C) * a.R * a.S * 4};
     const cuuint32_t bbox[3] = {32, 1, 32};
-    return ok && tiled_map(tb, c.B, 3, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    return tiled_map(tb, c.B, 3, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   const int Kg = a.N * a.P * a.Q;
-  const cuuint64_t ad[2] = {static_cast<cuuint64_t>(a.K), static_cast<cuuint64_t>(Kg)};
-  const cuuint64_t as[1] = {static_cast<cuuint64_t>(a.K) * 4};
-  const cuuint32_t abox[2] = {32, 32};
-  bool ok = tiled_map(ta, c.A, 2, ad, as, abox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  // A: dy as {co 32, pixel, co-block} (4 atoms per box) when Cout % 32 == 0
+  a.a_packed = 0;
+  bool ok = false;
+  if (a.K % 32 == 0) {
+    const cuuint64_t pd[3] = {32, static_cast<cuuint64_t>(Kg), static_cast<cuuint64_t>(a.K / 32)};
+    const cuuint64_t ps[2] = {static_cast<cuuint64_t>(a.K) * 4, 128};
+    const cuuint32_t pbox[3] = {32, 32, kBM / 32};
+    ok = tiled_map(ta, c.A, 3, pd, ps, pbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    a.a_packed = ok ? 1 : 0;
+  }
+  if (!ok) {
+    const cuuint64_t ad[2] = {static_cast<cuuint64_t>(a.K), static_cast<cuuint64_t>(Kg)};
+    const cuuint64_t as[1] = {static_cast<cuuint64_t>(a.K) * 4};
+    const cuuint32_t abox[2] = {32, 32};
+    if (!tiled_map(ta, c.A, 2, ad, as, abox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return false;
+  }
+  // B: 1x1 stride-1 unpadded convs read x as a plain {ci 32, pixel, ci-block} box
+  a.b_packed = 0;
+  if (a.R == 1 && a.S == 1 && a.stride == 1 && a.pad == 0) {
+    const cuuint64_t pd[3] = {32, static_cast<cuuint64_t>(Kg), static_cast<cuuint64_t>(a.C / 32)};
+    const cuuint64_t ps[2] = {static_cast<cuuint64_t>(a.C) * 4, 128};
+    const cuuint32_t pbox[3] = {32, 32, static_cast<cuuint32_t>(bn / 32)};
+    if (tiled_map(tb, c.B, 3, pd, ps, pbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      a.b_packed = 1;
+      return true;
+    }
+  }
   const int lo = -a.pad, up = a.pad - (a.R - 1);
-  return ok && im2col_map(tb, c.B, a.N, a.H, a.W, a.C, lo, lo, up, up, a.stride, 32,
-                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  return im2col_map(tb, c.B, a.N, a.H, a.W, a.C, lo, lo, up, up, a.stride, 32,
+                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 template <int MODE>
@@ -749,8 +809,8 @@ int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
 // -1: could not encode the tensor maps (not launched)
 int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   CUtensorMap ta, tb;
-  if (!encode(c, cfg.bn, &ta, &tb)) return -1;
   Prob a = c.a;
+  if (!encode(c, cfg.bn, &ta, &tb, a)) return -1;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (a.Ng + cfg.bn - 1) / cfg.bn;
   a.splits = cfg.splits;

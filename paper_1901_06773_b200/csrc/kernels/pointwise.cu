@@ -130,14 +130,16 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
 
   // ---- phase 1: per-block partial sums ----
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
-  float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0}, be[4] = {0, 0, 0, 0};
+  float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0};
+  float fsc[4] = {0, 0, 0, 0}, fsh[4] = {0, 0, 0, 0};  // forward scale / shift
   if (MODE == 1 && c_ok) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       mu[j] = a.mean[c + j];
       is[j] = a.invstd[c + j];
       ga[j] = a.gamma[c + j];
-      be[j] = a.beta[c + j];
+      fsc[j] = ga[j] * is[j];
+      fsh[j] = a.beta[c + j] - mu[j] * fsc[j];
     }
   }
   auto consume = [&](const float4 v, const float4 d, const float4 sk4) {
@@ -155,7 +157,8 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       for (int j = 0; j < 4; ++j) {
         const float xh = (xv[j] - mu[j]) * is[j];
         float g = dv[j];
-        if (a.relu && (xh * ga[j] + be[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
+        // the forward's pre-activation, bit for bit (scale/shift as in phase 2 of mode 0)
+        if (a.relu && (xv[j] * fsc[j] + fsh[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
         a0[j] += g;
         a1[j] += g * xh;
       }
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       for (int j = 0; j < 4; ++j) {
         const float xh = (xv[j] - mu[j]) * is[j];
         float g = dv[j];
-        if (a.relu && (xh * ga[j] + be[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
+        if (a.relu && (xv[j] * fsc[j] + fsh[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
         gg[j] = g;
         o[j] = k0[j] * (g - mg[j] - xh * mgx[j]);
       }
