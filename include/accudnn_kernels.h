@@ -53,6 +53,11 @@ int accudnn_conv_trace(void* buf);
  * timed with CUDA events and the fastest is cached for the process; 0: the
  * analytic choice.  Returns the previous setting. */
 int accudnn_conv_autotune(int enable);
+/* the autotuner's table as text (one "key[14] bn splits" line per shape;
+ * malloc'ed, release with free) and its inverse (merges, overwriting), so a
+ * tuned table can be shipped with a plan and runs are reproducible */
+int accudnn_conv_tune_export(char** text);
+int accudnn_conv_tune_import(const char* text);
 /* splits <= 0 picks a split-K factor automatically (TMA path: deterministic
  * workspace fix-up; cp.async fallback: fp32 atomics) */
 int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,

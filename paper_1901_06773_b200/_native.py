@@ -112,6 +112,8 @@ CUDA_SYMBOLS = {
     "accudnn_set_conv_impl": ([_I], _I),
     "accudnn_conv_set_workspace": ([ctypes.c_void_p, ctypes.c_ulonglong], _I),
     "accudnn_conv_autotune": ([_I], _I),
+    "accudnn_conv_tune_export": ([ctypes.POINTER(ctypes.c_void_p)], _I),
+    "accudnn_conv_tune_import": ([ctypes.c_char_p], _I),
     "accudnn_set_pdl": ([_I], _I),
     "accudnn_conv_trace": ([_P], _I),
     "accudnn_conv_fwd": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
@@ -149,3 +151,21 @@ def _declare_cuda(lib):
         _exec_symbols.declare(lib)
     except ImportError:
         pass
+
+
+def conv_tune_export():
+    """the conv autotuner's table (text, see include/accudnn_kernels.h)"""
+    import ctypes as _c
+    lib = cuda_lib()
+    p = _c.c_void_p()
+    if lib.accudnn_conv_tune_export(_c.byref(p)) != 0:
+        raise RuntimeError("accudnn_conv_tune_export failed")
+    try:
+        return _c.string_at(p).decode()
+    finally:
+        _c.CDLL(None).free(p)
+
+
+def conv_tune_import(text):
+    if cuda_lib().accudnn_conv_tune_import(text.encode()) != 0:
+        raise RuntimeError("accudnn_conv_tune_import failed")

@@ -37,6 +37,9 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <cstdlib>
+#include <sstream>
+#include <string>
 #include <unordered_map>
 #include <cstdio>
 #include <cstring>
@@ -1089,6 +1092,41 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
 // start of k-block i, [512,768) epilogue start/end of unit j); NULL = off
 extern "C" int accudnn_conv_trace(void* buf) {
   accudnn::g_trace = static_cast<long long*>(buf);
+  return 0;
+}
+
+// The tuned (BN, splits) table as text, one entry per line:
+// "k0 k1 ... k13 bn splits\n" (the 14-int shape key, see fill_key).  The
+// returned buffer is malloc'ed; release it with free() (accudnn_rt_free).
+extern "C" int accudnn_conv_tune_export(char** out) {
+  std::string t;
+  for (const auto& kv : accudnn::g_tuned) {
+    for (int v : kv.first) t += std::to_string(v) + " ";
+    t += std::to_string(kv.second.bn) + " " + std::to_string(kv.second.splits) + "\n";
+  }
+  char* buf = static_cast<char*>(std::malloc(t.size() + 1));
+  if (!buf) return static_cast<int>(cudaErrorMemoryAllocation);
+  std::memcpy(buf, t.c_str(), t.size() + 1);
+  *out = buf;
+  return 0;
+}
+// merges entries in the export format into the table (overwriting)
+extern "C" int accudnn_conv_tune_import(const char* text) {
+  if (!text) return static_cast<int>(cudaErrorInvalidValue);
+  std::istringstream in(text);
+  std::string line;
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    std::array<int, 14> key;
+    accudnn::Cfg cfg;
+    bool ok = true;
+    for (int& v : key) ok = ok && static_cast<bool>(ls >> v);
+    ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
+    if (!ok) continue;
+    if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;
+    if (cfg.splits < 1) continue;
+    accudnn::g_tuned[key] = cfg;
+  }
   return 0;
 }
 

@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
   // ---- phase 3: the block's rows again ----
   if (!c_ok) return;
   const int cl = lane_c * 4;
+  // last row of this thread's phase-1 sequence r_begin + lane_r + k*step
+  const long long first = r_begin + lane_r;
+  if (first >= r_end) return;
+  const long long r_hi = first + ((r_end - 1 - first) / step) * step;
   if (MODE == 0) {
     const float sc[4] = {coef[0][cl], coef[0][cl + 1], coef[0][cl + 2], coef[0][cl + 3]};
     const float sh[4] = {coef[1][cl], coef[1][cl + 1], coef[1][cl + 2], coef[1][cl + 3]};
@@ -321,19 +325,20 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       }
       return v;
     };
-    long long r = r_begin + lane_r;
-    for (; r + 3 * step < r_end; r += 4 * step) {
+    // rows in reverse: the lines read last in phase 1 are the likeliest L2 hits
+    long long r = r_hi;
+    for (; r - 3 * step >= r_begin; r -= 4 * step) {
       float4 v[4], kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
-        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r + u * step) * C + c)) : v[u];
+        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r - u * step) * C + c));
+        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r - u * step) * C + c)) : v[u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        *reinterpret_cast<float4*>(a.y + (r + u * step) * C + c) = f(v[u], kv[u]);
+        *reinterpret_cast<float4*>(a.y + (r - u * step) * C + c) = f(v[u], kv[u]);
     }
-    for (; r < r_end; r += step) {
+    for (; r >= r_begin; r -= step) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
       *reinterpret_cast<float4*>(a.y + r * C + c) =
           f(v, SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v);
@@ -374,19 +379,19 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       put(a.dx, o, a.dx_beta);
       if (SKIP) put(a.dskip, gg, a.dskip_beta);  // d(shortcut) = masked dy
     };
-    long long r = r_begin + lane_r;
-    for (; r + 3 * step < r_end; r += 4 * step) {
+    long long r = r_hi;  // reverse order, as above
+    for (; r - 3 * step >= r_begin; r -= 4 * step) {
       float4 xv[4], dv[4], kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        xv[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
-        dv[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * C + c));
-        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r + u * step) * C + c)) : xv[u];
+        xv[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r - u * step) * C + c));
+        dv[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r - u * step) * C + c));
+        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r - u * step) * C + c)) : xv[u];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], kv[u], r + u * step);
+      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], kv[u], r - u * step);
     }
-    for (; r < r_end; r += step) {
+    for (; r >= r_begin; r -= step) {
       const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
       f(xv, __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)),
         SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : xv, r);

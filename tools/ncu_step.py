@@ -16,6 +16,10 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 27
 warm = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 image, classes = (224, 1000) if arch in ("resnet50", "resnet101", "resnet152") else (32, 12)
 _, desc = trainer.export_network(arch, image, classes)
+_tune = os.path.join(ROOT, "profiles", "b200", "conv_tune.txt")
+if os.path.exists(_tune):
+    from paper_1901_06773_b200 import _native
+    _native.conv_tune_import(open(_tune).read())
 ex = trainer.Executor(arch, image, classes, k=k)
 ex.set_params(trainer.init_params(desc, 0))
 g = np.random.default_rng(0)

@@ -23,6 +23,10 @@ _, desc = trainer.export_network(arch, image, classes)
 # predecessor: per-kernel durations are only meaningful with ACCUDNN_PDL=0
 if "ACCUDNN_PDL" in os.environ:
     trainer._lib().accudnn_set_pdl(int(os.environ["ACCUDNN_PDL"]))
+_tune = os.path.join(ROOT, "profiles", "b200", "conv_tune.txt")
+if os.path.exists(_tune):
+    from paper_1901_06773_b200 import _native
+    _native.conv_tune_import(open(_tune).read())
 ex = trainer.Executor(arch, image, classes, k=k)
 ex.set_params(trainer.init_params(desc, 0))
 ex.set_graph(True)
