@@ -173,7 +173,7 @@ def roofline_from_trace(desc, trace_csv, k, peak_tflops, n_ops):
     achieved = conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
     return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_tflops,
             "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4), "traffic": None,
-            "kernel": "conv_igemm_kernel (tcgen05 kind::tf32)",
+            "kernel": "conv_sm100_kernel (persistent, TMA + tcgen05 kind::tf32, TMEM accumulators)",
             "conv_share_of_step": round(conv_ms / total_ms, 4) if total_ms else None,
             "flops_per_launch_note": "sum of conv/fc fwd+dgrad+wgrad FLOPs per step / sum of "
                                      "their phase times (CUDA events on the compute stream)"}
@@ -359,6 +359,17 @@ def run_ours(args):
     roof = roofline_from_trace(desc, trace, k, tf32_peak, len(desc["ops"]))
     roof["peak_note"] = ("TF32 dense peak taken as 1/2 of the measured cuBLAS bf16 sustained "
                          "figure in MEASURED_PEAKS.json (nominal 1.1 vs 2.25 PF)")
+    # DRAM traffic of the conv kernels per launch, from the committed ncu
+    # launch list of the same step (profiles/r01, dram__bytes_read+write)
+    ls_path = os.path.join(ROOT, "profiles", "r01", f"launch_summary_k{k}.json")
+    if os.path.exists(ls_path):
+        summ = json.load(open(ls_path))
+        cv = [v for n, v in summ.items() if "conv_sm100_kernel" in n or "conv_igemm_kernel" in n]
+        n_launch = sum(v["launches"] for v in cv)
+        if n_launch:
+            roof["traffic"] = round(sum(v["dram_bytes"] for v in cv) / n_launch)
+            roof["traffic_unit"] = "DRAM bytes per conv launch (ncu, cold cache, serialised)"
+            roof["algorithmic_flops_per_launch"] = round(k * conv_flops_per_image(desc) / n_launch)
     arena, fixed = ex.memory()
     f_conv = conv_flops_per_image(desc)
     swapped = prof["swapped_bytes"]
