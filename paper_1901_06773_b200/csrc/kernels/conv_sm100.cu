@@ -17,8 +17,9 @@
 //          A: 2-D MN-major tiles of dy [pixels][Cout]; B: im2col TMA of x with
 //          32 output pixels per column (MN-major)
 //
-// Kernel structure (192 threads, one CTA per SM, persistent):
-//   warp 0     TMA producer (one elected thread) over a STAGES-deep smem ring
+// Kernel structure (224 threads, one CTA per SM, persistent):
+//   warps 0, 6 TMA producers (one thread each, alternate k-blocks) over a
+//              STAGES-deep smem ring
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5  epilogue: TMEM -> registers -> HBM
 // The CTA walks work units u = blockIdx.x + i*gridDim.x; a unit is one
@@ -53,7 +54,11 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;
-constexpr int kThreads = 192;
+// warp 0 and warps 6.. issue TMA loads (k-block kc by producer kc % kProducers):
+// one thread issues a stage every ~240-480 cycles (a TMA instruction blocks
+// its issuer ~120-240 cycles), so two issuers keep the ring full
+constexpr int kProducers = 2;
+constexpr int kThreads = 192 + 32 * (kProducers - 1);
 constexpr int kEpiThreads = 128;
 
 enum Mode : int { FWD = 0, DGRAD = 1, WGRAD = 2 };
@@ -229,10 +234,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 769] = gtimer();
 
-  if (warp == 0) {
+  if (warp == 0 || warp >= 6) {
     if (lane == 0) {
-      // ============================ TMA producer ============================
-      uint32_t kc = 0;  // k-blocks issued by this CTA (ring position)
+      // ============================ TMA producers ============================
+      const uint32_t pid = warp == 0 ? 0u : static_cast<uint32_t>(warp - 5);
+      uint32_t kc = 0;  // k-blocks of this CTA (ring position)
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const int split = u % a.splits;
         const int tile = u / a.splits;
@@ -259,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           wt_s = tap - wt_r * a.S;
         }
         for (int kb = kb0; kb < kb1; ++kb, ++kc) {
+          if (kc % kProducers != pid) continue;
           const uint32_t stage = kc % STAGES;
           if (kc >= STAGES) ptx::mbar_wait(&empty[stage], ((kc / STAGES) - 1) & 1);
           if (a.trace && kc < 256) a.trace[blockIdx.x * 1024 + kc] = clock64();

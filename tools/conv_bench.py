@@ -24,11 +24,27 @@ def shapes(k):
     return seen
 
 
-def timeit(fn, iters=20):
+def timeit(fn, iters=20, graph=False):
+    """device time per call; graph=True replays `iters` calls captured in a
+    CUDA graph (no host launch/encode cost, as inside the training step)"""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if graph:
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(iters):
+                    fn(s)
+            g.replay()
+            torch.cuda.synchronize()
+            a.record(s)
+            g.replay()
+            b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / iters
     a.record()
     for _ in range(iters):
         fn()
@@ -40,6 +56,11 @@ def timeit(fn, iters=20):
 def main():
     k = int(sys.argv[1]) if len(sys.argv) > 1 else 27
     lib = _native.cuda_lib()
+    import os
+    tune = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "b200",
+                        "conv_tune.txt")
+    if os.path.exists(tune):
+        _native.conv_tune_import(open(tune).read())
     dev = torch.device("cuda:0")
     torch.backends.cudnn.allow_tf32 = True
     torch.backends.cuda.matmul.allow_tf32 = True
@@ -62,17 +83,18 @@ def main():
         wc = wt.permute(0, 3, 1, 2)
         dyc = dy.permute(0, 3, 1, 2)
         res = {"shape": f"{h}x{w} {c}->{kk} r{r} s{st}", "count": count}
+        S = lambda s: ctypes.c_void_p(s.cuda_stream) if s is not None else None  # noqa: E731
         for mode, fn, cfn in (
-            ("fwd", lambda: lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), wt.data_ptr(), y.data_ptr(), 0, None),
-             lambda: torch.nn.functional.conv2d(xc, wc, stride=st, padding=pad)),
-            ("dgrad", lambda: lib.accudnn_conv_dgrad(ctypes.byref(d), dy.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, None),
-             lambda: torch.ops.aten.convolution_backward(dyc, xc, wc, None, [st, st], [pad, pad], [1, 1], False, [0, 0], 1, [True, False, False])),
-            ("wgrad", lambda: lib.accudnn_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, 0, None),
-             lambda: torch.ops.aten.convolution_backward(dyc, xc, wc, None, [st, st], [pad, pad], [1, 1], False, [0, 0], 1, [False, True, False]))):
+            ("fwd", lambda s=None: lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), wt.data_ptr(), y.data_ptr(), 0, S(s)),
+             lambda s=None: torch.nn.functional.conv2d(xc, wc, stride=st, padding=pad)),
+            ("dgrad", lambda s=None: lib.accudnn_conv_dgrad(ctypes.byref(d), dy.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, S(s)),
+             lambda s=None: torch.ops.aten.convolution_backward(dyc, xc, wc, None, [st, st], [pad, pad], [1, 1], False, [0, 0], 1, [True, False, False])),
+            ("wgrad", lambda s=None: lib.accudnn_conv_wgrad(ctypes.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, 0, S(s)),
+             lambda s=None: torch.ops.aten.convolution_backward(dyc, xc, wc, None, [st, st], [pad, pad], [1, 1], False, [0, 0], 1, [False, True, False]))):
             if mode == "dgrad" and x.shape[-1] == 4:
                 continue
-            ms = timeit(fn)
-            cms = timeit(cfn)
+            ms = timeit(fn, graph=True)
+            cms = timeit(cfn, graph=True)
             res[mode] = {"ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1),
                          "cudnn_ms": round(cms, 4), "cudnn_tflops": round(flops / cms / 1e9, 1)}
             tot["ours"] += ms * count

@@ -13,6 +13,11 @@ from paper_1901_06773_b200 import _native  # noqa: E402
 mode = sys.argv[1]
 n, c, h, w, k, r, st, pad = (int(v) for v in sys.argv[2:10])
 lib = _native.cuda_lib()
+import os  # noqa: E402
+_tune = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "b200",
+                     "conv_tune.txt")
+if os.path.exists(_tune):
+    _native.conv_tune_import(open(_tune).read())
 p = (h + 2 * pad - r) // st + 1
 q = (w + 2 * pad - r) // st + 1
 d = _native.ConvDesc(n, h, w, c, k, r, r, st, pad, p, q)
