@@ -116,6 +116,7 @@ CUDA_SYMBOLS = {
     "accudnn_conv_tune_import": ([ctypes.c_char_p], _I),
     "accudnn_set_pdl": ([_I], _I),
     "accudnn_conv_trace": ([_P], _I),
+    "accudnn_bn_trace": ([_P], _I),
     "accudnn_conv_fwd": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_dgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_wgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _I, _P], _I),

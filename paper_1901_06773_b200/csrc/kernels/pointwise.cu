@@ -51,7 +51,7 @@ int grid_for(long long work, int per_block, int cap = 148 * 16) {
 constexpr int kBnThreads = 512;
 constexpr int kBnGroup = 128;        // channels per channel group
 constexpr int kBnMaxBlocks = 1024;   // gx * Y
-constexpr int kBnMaxGroups = 64;     // C <= 8192
+constexpr int kBnMaxGroups = 256;    // 32-channel groups: C <= 8192
 constexpr int kBnCounters = 64;
 
 struct BnWs {
@@ -88,8 +88,23 @@ struct BnArgs {
   float* dskip;          // SKIP, mode 1: gradient of the shortcut (+= when dskip_beta)
   int dskip_beta;
   BnWs w;
+  long long* trace;      // debug: globaltimer stamps per block (accudnn_bn_trace)
 };
+long long* g_bn_trace = nullptr;
+__device__ __forceinline__ long long bn_gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BN_STAMP(i)                                                                     \
+  do {                                                                                  \
+    if (a.trace && threadIdx.x == 0)                                                    \
+      a.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (i)] = bn_gtimer();           \
+  } while (0)
 
+// grid-wide barrier (all blocks co-resident: cooperative launch):
+// counters[0] arrivals, counters[1] generation.  (Measured: one barrier over
+// the grid is faster than per-channel-group barriers here.)
 __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblocks) {
   __threadfence();
   __syncthreads();
@@ -112,6 +127,7 @@ template <int MODE, bool CLUSTER, bool SKIP>
 __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel(const BnArgs a) {
   pdl_wait();
   pdl_trigger();
+  BN_STAMP(0);
   __shared__ float red[2][kBnThreads][4];
   __shared__ __align__(16) float cpart[2][kBnGroup];  // CLUSTER: this block's partial
   __shared__ double dsum[kBnThreads];
@@ -188,36 +204,71 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       consume(v, d, sk);
     }
   }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    red[0][threadIdx.x][j] = a0[j];
-    red[1][threadIdx.x][j] = a1[j];
-  }
-  __syncthreads();
+  BN_STAMP(1);
   const int gx = gridDim.x;
-  // fixed-shape tree over the row lanes
-  for (int n = rows_per_pass; n > 1;) {
-    const int half = (n + 1) / 2;
-    if (lane_r < n - half) {
-      const int src = (lane_r + half) * lanes + lane_c;
+  float* slot = CLUSTER ? &cpart[0][0]
+                        : a.w.part + static_cast<size_t>(blockIdx.y * gx + blockIdx.x) * 2 * kBnGroup;
+  if (32 % lanes == 0) {
+    // row lanes of a warp: fixed xor-shuffle tree, then the 16 warp partials
+    // summed in warp order by `lanes` threads (one barrier)
+    for (int off = lanes; off < 32; off <<= 1) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        red[0][threadIdx.x][j] += red[0][src][j];
-        red[1][threadIdx.x][j] += red[1][src][j];
+        a0[j] += __shfl_xor_sync(0xffffffffu, a0[j], off);
+        a1[j] += __shfl_xor_sync(0xffffffffu, a1[j], off);
       }
     }
-    n = half;
+    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (ln < lanes) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        red[0][wid * lanes + ln][j] = a0[j];
+        red[1][wid * lanes + ln][j] = a1[j];
+      }
+    }
     __syncthreads();
-  }
-  if (lane_r == 0) {
-    float* slot = CLUSTER ? &cpart[0][0]
-                          : a.w.part + static_cast<size_t>(blockIdx.y * gx + blockIdx.x) * 2 * kBnGroup;
-    *reinterpret_cast<float4*>(slot + lane_c * 4) =
-        make_float4(red[0][lane_c][0], red[0][lane_c][1], red[0][lane_c][2], red[0][lane_c][3]);
-    *reinterpret_cast<float4*>(slot + kBnGroup + lane_c * 4) =
-        make_float4(red[1][lane_c][0], red[1][lane_c][1], red[1][lane_c][2], red[1][lane_c][3]);
+    if (threadIdx.x < lanes) {
+      float t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
+      for (int w = 0; w < kBnThreads / 32; ++w)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          t0[j] += red[0][w * lanes + threadIdx.x][j];
+          t1[j] += red[1][w * lanes + threadIdx.x][j];
+        }
+      *reinterpret_cast<float4*>(slot + threadIdx.x * 4) = make_float4(t0[0], t0[1], t0[2], t0[3]);
+      *reinterpret_cast<float4*>(slot + kBnGroup + threadIdx.x * 4) =
+          make_float4(t1[0], t1[1], t1[2], t1[3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      red[0][threadIdx.x][j] = a0[j];
+      red[1][threadIdx.x][j] = a1[j];
+    }
+    __syncthreads();
+    // fixed-shape tree over the row lanes
+    for (int n = rows_per_pass; n > 1;) {
+      const int half = (n + 1) / 2;
+      if (lane_r < n - half) {
+        const int src = (lane_r + half) * lanes + lane_c;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          red[0][threadIdx.x][j] += red[0][src][j];
+          red[1][threadIdx.x][j] += red[1][src][j];
+        }
+      }
+      n = half;
+      __syncthreads();
+    }
+    if (lane_r == 0) {
+      *reinterpret_cast<float4*>(slot + lane_c * 4) =
+          make_float4(red[0][lane_c][0], red[0][lane_c][1], red[0][lane_c][2], red[0][lane_c][3]);
+      *reinterpret_cast<float4*>(slot + kBnGroup + lane_c * 4) =
+          make_float4(red[1][lane_c][0], red[1][lane_c][1], red[1][lane_c][2], red[1][lane_c][3]);
+    }
   }
 
+  BN_STAMP(2);
   const int ch = lanes * 4;  // channels of this group
   const int V = 2 * ch;      // values: sum1 of ch channels, then sum2
   int T = 1;
@@ -296,6 +347,7 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
   }
   __syncthreads();
 
+  BN_STAMP(3);
   // ---- phase 3: the block's rows again ----
   if (!c_ok) return;
   const int cl = lane_c * 4;
@@ -343,6 +395,7 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       *reinterpret_cast<float4*>(a.y + r * C + c) =
           f(v, SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v);
     }
+    BN_STAMP(4);
   } else {
     float mg[4], mgx[4], k0[4];
 #pragma unroll
@@ -396,6 +449,7 @@ __global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel
       f(xv, __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)),
         SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : xv, r);
     }
+    BN_STAMP(4);
   }
 }
 
@@ -863,6 +917,14 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, int n, int c, i
 
 using namespace accudnn;
 
+// debug: subsequent BN launches stamp %globaltimer per block into buf
+// (8 int64 per block: entry, phase-1 loop done, partial published, phase 2
+// done, phase 3 done); NULL = off
+extern "C" int accudnn_bn_trace(void* buf) {
+  accudnn::g_bn_trace = static_cast<long long*>(buf);
+  return 0;
+}
+
 extern "C" int accudnn_set_pdl(int enable) {
   const int prev = accudnn::g_pdl;
   accudnn::g_pdl = enable ? 1 : 0;
@@ -877,7 +939,7 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
                               const float* beta, float eps, int relu, float* y,
                               float* save_mean, float* save_invstd, float* running_mean,
                               float* running_var, float momentum, void* ws, void* stream) {
-  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
+  if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   BnArgs a{};
   a.x = x;
   a.M = M;
@@ -893,6 +955,7 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
   a.run_var = running_var;
   a.y = y;
   a.w = bn_ws(ws, C);
+  a.trace = g_bn_trace;
   return bn_launch<0, false>(a, S(stream));
 }
 
@@ -900,7 +963,7 @@ extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int 
                               const float* gamma, const float* beta, const float* save_mean,
                               const float* save_invstd, int relu, float* dx, int dx_beta,
                               float* dgamma, float* dbeta, void* ws, void* stream) {
-  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
+  if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   BnArgs a{};
   a.x = x;
   a.dy = dy;
@@ -916,6 +979,7 @@ extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int 
   a.dx = dx;
   a.dx_beta = dx_beta;
   a.w = bn_ws(ws, C);
+  a.trace = g_bn_trace;
   return bn_launch<1, false>(a, S(stream));
 }
 
@@ -925,7 +989,7 @@ extern "C" int accudnn_bn_add_relu_fwd(const float* x, const float* skip, long l
                                        float* save_mean, float* save_invstd, float* running_mean,
                                        float* running_var, float momentum, void* ws,
                                        void* stream) {
-  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
+  if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   BnArgs a{};
   a.x = x;
   a.skip = skip;
@@ -952,7 +1016,7 @@ extern "C" int accudnn_bn_add_relu_bwd(const float* x, const float* skip, const 
                                        const float* save_mean, const float* save_invstd,
                                        float* dx, int dx_beta, float* dskip, int dskip_beta,
                                        float* dgamma, float* dbeta, void* ws, void* stream) {
-  if ((C & 3) || M <= 0 || C > kBnGroup * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
+  if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   BnArgs a{};
   a.x = x;
   a.skip = skip;

@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python -m pytest tests/test_layers_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python tools/bn_bench.py 42 > gpurun_out/bn_bench.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1
-cp gpurun_out/conv_tune.txt profiles/b200/conv_tune.txt
-timeout 600 python bench.py > gpurun_out/bench2.log 2>&1
