@@ -124,7 +124,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
 }
 
 template <int MODE, bool CLUSTER, bool SKIP>
-__global__ void __launch_bounds__(kBnThreads, MODE == 0 ? 2 : 1) bn_fused_kernel(const BnArgs a) {
+__global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) ? 2 : 1) bn_fused_kernel(const BnArgs a) {
   pdl_wait();
   pdl_trigger();
   BN_STAMP(0);
