@@ -430,11 +430,17 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   };
 
   // wait for everything a newly written instance's region depends on
+  // phases whose compute waited on a copy stream (prefetch landed / offload
+  // drained): the only gaps that count as exposed swap time
+  std::vector<char> swap_wait(static_cast<size_t>(2 * n + 2), 0);
+  int cur_step = 0;
   auto wait_region = [&](int inst, cudaStream_t stream, bool same_as_compute) {
     for (int p : I.preds[static_cast<size_t>(inst)]) {
       const Instance& y = I.lm.inst[static_cast<size_t>(p)];
-      if (y.kind == InstKind::act && y.swapped)
+      if (y.kind == InstKind::act && y.swapped) {
         ck(cudaStreamWaitEvent(stream, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
+        if (same_as_compute) swap_wait[static_cast<size_t>(cur_step)] = 1;
+      }
       if (!same_as_compute) {
         ck(cudaStreamWaitEvent(stream, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
       }
@@ -512,9 +518,12 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
         // previous iteration's prefetch, which stream capture rejects)
         if (!fwd && bwd_reads_input(op))
           for (int x : {op.in0, op.in1})
-            if (x >= 0 && I.swapped[static_cast<size_t>(x)])
+            if (x >= 0 && I.swapped[static_cast<size_t>(x)]) {
               ck(cudaStreamWaitEvent(cs, I.h2d_done[static_cast<size_t>(x)], 0), "wait");
+              swap_wait[static_cast<size_t>(s)] = 1;
+            }
       }
+      cur_step = s;
       for (int inst : I.first_compute_write[static_cast<size_t>(s)]) wait_region(inst, cs, true);
       if (profile && !capture) ck(cudaEventRecord(I.phase_begin[static_cast<size_t>(s)], cs), "rec");
       for (int o : ops) {
@@ -616,22 +625,24 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       st.swapped_bytes += static_cast<unsigned long long>(
           I.lm.inst[static_cast<size_t>(I.lm.act_inst[static_cast<size_t>(t)])].bytes);
   if (profile) {
-    // exposed swap time: compute-stream gaps between consecutive phases
-    double busy = 0;
-    std::string tr = "phase,begin_ms,end_ms\n";
+    // exposed swap time: the compute-stream gaps in front of the phases that
+    // waited on a copy stream (prefetch not landed / region not drained);
+    // gaps elsewhere are launch latency of the eager profiled step
+    std::string tr = "phase,begin_ms,end_ms,swap_wait\n";
+    double exposed = 0;
+    float prev_e = 0;
     for (int s = 1; s <= 2 * n; ++s) {
       float b = 0, e = 0;
       ck(cudaEventElapsedTime(&b, I.iter_begin, I.phase_begin[static_cast<size_t>(s)]), "t");
       ck(cudaEventElapsedTime(&e, I.iter_begin, I.phase_end[static_cast<size_t>(s)]), "t");
-      busy += e - b;
-      char line[96];
-      std::snprintf(line, sizeof line, "%d,%.6f,%.6f\n", s, b, e);
+      if (s > 1 && swap_wait[static_cast<size_t>(s)]) exposed += std::max(0.f, b - prev_e);
+      prev_e = e;
+      char line[112];
+      std::snprintf(line, sizeof line, "%d,%.6f,%.6f,%d\n", s, b, e,
+                    static_cast<int>(swap_wait[static_cast<size_t>(s)]));
       tr += line;
     }
-    float first_b = 0, last_e = 0;
-    ck(cudaEventElapsedTime(&first_b, I.iter_begin, I.phase_begin[1]), "t");
-    ck(cudaEventElapsedTime(&last_e, I.iter_begin, I.phase_end[static_cast<size_t>(2 * n)]), "t");
-    st.exposed_swap_ms = std::max(0.0, (last_e - first_b) - busy);
+    st.exposed_swap_ms = exposed;
     trace_ = tr;
   }
   return st;

@@ -48,12 +48,15 @@ if not kern:
     print("no kernel events captured")
     sys.exit(1)
 span = kern[-1][1] - kern[0][0]
-busy, last_end, gaps = 0.0, kern[0][0], []
-for s, e, _ in kern:
+busy, last_end, gaps, big = 0.0, kern[0][0], [], []
+prev = ""
+for s, e, nm in kern:
     if s > last_end:
         gaps.append(s - last_end)
+        big.append((s - last_end, prev[:50], nm[:50]))
     busy += max(0.0, e - max(s, last_end))
     last_end = max(last_end, e)
+    prev = nm
 agg = collections.defaultdict(lambda: [0, 0.0])
 for s, e, n in kern:
     key = n.replace("(anonymous namespace)::", "").replace("accudnn::", "").replace("void ", "")
@@ -68,6 +71,9 @@ res = {"arch": arch, "k": k, "steps": steps, "kernels_per_step": len(kern) / ste
        "top": sorted(([n, c // steps, round(t / steps / 1e3, 3), round(t / c, 2)]
                       for n, (c, t) in agg.items()), key=lambda r: -r[2])[:25]}
 print(json.dumps({k_: v for k_, v in res.items() if k_ != "top"}, indent=1))
+print("largest gaps (us, before -> after):")
+for gp in sorted(big, reverse=True)[:8]:
+    print("  %.1f  %s -> %s" % gp)
 print("kernel | launches/step | ms/step | us/launch")
 for r in res["top"]:
     print(" | ".join(str(v) for v in r))
