@@ -875,9 +875,9 @@ Cfg model_cfg(const Call& c) {
 }
 
 // Empirical choice of (BN, splits) for one GEMM: every candidate is run
-// once and then timed (min of 3, CUDA events on the caller's stream).  Only
-// outputs that are overwritten (beta = 0) are tuned, never during stream
-// capture; the result is cached per shape for the life of the process.
+// once and then timed (min of 3, CUDA events on the caller's stream), never
+// during stream capture; accumulating (beta = 1) calls are tuned on a scratch
+// output.  The result is cached per shape for the life of the process.
 Cfg tune(const Call& c, cudaStream_t st) {
   static const int kSplits[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64, 96, 128};
   cudaEvent_t e0, e1;
@@ -925,9 +925,29 @@ int run_call(const Call& c, cudaStream_t st) {
   } else {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cap);
-    if (g_autotune && !c.a.beta && cap == cudaStreamCaptureStatusNone) {
-      cfg = tune(c, st);
-      g_tuned[key] = cfg;
+    if (g_autotune && cap == cudaStreamCaptureStatusNone) {
+      if (!c.a.beta) {
+        cfg = tune(c, st);
+        g_tuned[key] = cfg;
+      } else {
+        // accumulating calls are tuned against a scratch copy of the output
+        // (the candidates add into it; the real output is left untouched)
+        const size_t out_bytes =
+            sizeof(float) * (c.mode == DGRAD ? static_cast<size_t>(c.a.N) * c.a.H * c.a.W * c.a.C
+                                             : static_cast<size_t>(c.a.M) * c.a.Ng);
+        float* scratch = nullptr;
+        if (cudaMalloc(&scratch, out_bytes) == cudaSuccess) {
+          Call c2 = c;
+          c2.a.out = scratch;
+          cfg = tune(c2, st);
+          cudaStreamSynchronize(st);
+          cudaFree(scratch);
+          g_tuned[key] = cfg;
+        } else {
+          cudaGetLastError();
+          cfg = model_cfg(c);
+        }
+      }
     } else {
       cfg = model_cfg(c);
     }
