@@ -58,6 +58,10 @@ int accudnn_conv_autotune(int enable);
  * tuned table can be shipped with a plan and runs are reproducible */
 int accudnn_conv_tune_export(char** text);
 int accudnn_conv_tune_import(const char* text);
+/* test hook: force tile width (64/128/256), split-K factor and cluster size
+ * (1, or 2 = B tile multicast across an M-tile pair) for every TMA conv
+ * launch; 0 fields = automatic */
+int accudnn_conv_force_cfg(int bn, int splits, int cm);
 /* splits <= 0 picks a split-K factor automatically (TMA path: deterministic
  * workspace fix-up; cp.async fallback: fp32 atomics) */
 int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,

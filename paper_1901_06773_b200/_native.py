@@ -114,6 +114,7 @@ CUDA_SYMBOLS = {
     "accudnn_conv_autotune": ([_I], _I),
     "accudnn_conv_tune_export": ([ctypes.POINTER(ctypes.c_void_p)], _I),
     "accudnn_conv_tune_import": ([ctypes.c_char_p], _I),
+    "accudnn_conv_force_cfg": ([_I, _I, _I], _I),
     "accudnn_set_pdl": ([_I], _I),
     "accudnn_conv_trace": ([_P], _I),
     "accudnn_bn_trace": ([_P], _I),

@@ -113,6 +113,52 @@ __device__ __forceinline__ void tma_4d(const CUtensorMap* tm, uint32_t dst, uint
       "r"(c3)
       : "memory");
 }
+// multicast variants: the box lands at the same smem offset in every CTA of
+// `mask` and completes tx bytes on each destination's barrier at `bar`'s offset
+__device__ __forceinline__ void tma_2d_mc(const CUtensorMap* tm, uint32_t dst, uint64_t* bar,
+                                          int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_mc(const CUtensorMap* tm, uint32_t dst, uint64_t* bar,
+                                          int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d_mc(const CUtensorMap* tm, uint32_t dst, uint64_t* bar,
+                                          int c0, int c1, int c2, int c3, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3), "h"(mask)
+      : "memory");
+}
+// arrive on `bar` (same offset) in every CTA of `mask` when this thread's
+// previously issued tcgen05.mma complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(ptx::smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
 __device__ __forceinline__ void tma_im2col(const CUtensorMap* tm, uint32_t dst, uint64_t* bar,
                                            int c, int w, int h, int n, uint16_t ow, uint16_t oh) {
   asm volatile(
@@ -184,7 +230,10 @@ __device__ __forceinline__ long long out_row(const Prob& a, int m) {
   return ((static_cast<long long>(n) * a.H + h) * a.W + w) * a.C;
 }
 
-template <int MODE, int BN, int STAGES>
+// CM = 2: a cluster of two CTAs on adjacent M-tiles of the same N-tile; each
+// loads its own A and half of B, multicasting the B half to both (B traffic
+// from L2 halves); both MMA warps release a stage on both CTAs
+template <int MODE, int BN, int STAGES, int CM>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
@@ -208,11 +257,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 768] = gtimer();
+  const uint32_t crank = CM > 1 ? cluster_ctarank() : 0u;
+  const int cid = static_cast<int>(blockIdx.x) / CM;     // cluster index
+  const int ncl = static_cast<int>(gridDim.x) / CM;      // clusters in the grid
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CM) - 1u);
+  // work unit -> (split, m-tile, n-tile); with CM = 2 the unit is a tile pair
+  auto decode = [&](int u, int& split, int& tile, int& tm, int& tn) {
+    split = u % a.splits;
+    const int pair = u / a.splits;
+    if (CM == 1) {
+      tile = pair;
+      tm = pair % a.tiles_m;
+      tn = pair / a.tiles_m;
+    } else {
+      const int tiles_m2 = (a.tiles_m + 1) / 2;
+      tm = (pair % tiles_m2) * 2 + static_cast<int>(crank);
+      tn = pair / tiles_m2;
+      tile = tn * a.tiles_m + tm;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], CM);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
@@ -225,7 +293,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CM > 1)
+    cluster_sync_all();  // peers' barriers initialised before any multicast / remote arrive
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t smem_base = ptx::smem_u32(smem);
@@ -239,11 +310,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ============================ TMA producers ============================
       const uint32_t pid = warp == 0 ? 0u : static_cast<uint32_t>(warp - 5);
       uint32_t kc = 0;  // k-blocks of this CTA (ring position)
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-        const int split = u % a.splits;
-        const int tile = u / a.splits;
-        const int tm = tile % a.tiles_m;
-        const int tn = tile / a.tiles_m;
+      for (int u = cid; u < a.units; u += ncl) {
+        int split, tile, tm, tn;
+        decode(u, split, tile, tm, tn);
         const int m0 = tm * kBM, n0 = tn * BN;
         const int kb0 = split * a.kb_per_split;
         const int kb1 = min(a.kb_total, kb0 + a.kb_per_split);
@@ -283,7 +352,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_im2col(&tmA, sA, bar, c0, pj * a.stride - a.pad, pi * a.stride - a.pad, pn,
                          static_cast<uint16_t>(s), static_cast<uint16_t>(r));
             }
-            tma_2d(&tmB, sB, bar, kk, n0);
+            if (CM > 1)
+              tma_2d_mc(&tmB, sB + crank * (kBBytes / CM), bar, kk,
+                        n0 + static_cast<int>(crank) * (BN / CM), kMask);
+            else
+              tma_2d(&tmB, sB, bar, kk, n0);
           } else if constexpr (MODE == DGRAD) {
             const int t = kk / a.K, co0 = kk - t * a.K;
             const int tr = t / a.Sc, ts = t - tr * a.Sc;
@@ -294,7 +367,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_im2col(&tmA, sA, bar, co0, pj + a.lo_w, pi + a.lo_h, pn,
                          static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
             }
-            if (a.b_packed) {  // {ci 32, co, ci-block, tap}: all BN/32 atoms at once
+            if (CM > 1) {  // this CTA's half of the atoms, multicast to the pair
+              constexpr int kHalf = BN / 32 / CM;
+              const int b0 = static_cast<int>(crank) * kHalf;
+              if (a.b_packed) {
+                tma_4d_mc(&tmB, sB + b0 * 4096, bar, 0, co0, n0 / 32 + b0, tap, kMask);
+              } else {
+#pragma unroll
+                for (int b = 0; b < kHalf; ++b)
+                  tma_3d_mc(&tmB, sB + (b0 + b) * 4096, bar, n0 + 32 * (b0 + b), tap, co0, kMask);
+              }
+            } else if (a.b_packed) {  // {ci 32, co, ci-block, tap}: all BN/32 atoms at once
               tma_4d(&tmB, sB, bar, 0, co0, n0 / 32, tap);
             } else {
 #pragma unroll
@@ -330,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = ptx::idesc_tf32(kBM, BN, kAmn, kBmn);
       uint32_t kc = 0;
       int j = 0;  // units processed by this CTA
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++j) {
+      for (int u = cid; u < a.units; u += ncl, ++j) {
         const int split = u % a.splits;
         const int kb0 = split * a.kb_per_split;
         const int kb1 = min(a.kb_total, kb0 + a.kb_per_split);
@@ -353,7 +436,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : ptx::smem_desc(sB + ks * 32, 16, 1024, 2);
             ptx::mma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[stage]);
+          if (CM > 1)
+            mma_commit_mc(&empty[stage], kMask);  // the stage holds the peer's B half too
+          else
+            ptx::mma_commit(&empty[stage]);
         }
         ptx::mma_commit(&tfull[acc]);
       }
@@ -375,11 +461,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gg = lane & 7;      // read-back 16-byte granule
     uint32_t nchunk = 0;          // chunks staged by this warp (buffer parity)
     int j = 0;
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++j) {
-      const int split = u % a.splits;
-      const int tile = u / a.splits;
-      const int tm = tile % a.tiles_m;
-      const int tn = tile / a.tiles_m;
+    for (int u = cid; u < a.units; u += ncl, ++j) {
+      int split, tile, tm, tn;
+      decode(u, split, tile, tm, tn);
       const int m0 = tm * kBM + quad * 32, n0 = tn * BN;
       const int acc = j & 1;
       ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
@@ -462,7 +546,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CM > 1)
+    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
+  else
+    __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem);
@@ -636,21 +723,35 @@ int choose_splits(long long tiles, int kb_total, int bn, long long out_elems, in
   return best;
 }
 
-template <int MODE, int BN, int STAGES>
+template <int MODE, int BN, int STAGES, int CM>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
              cudaStream_t st) {
   constexpr size_t smem = STAGES * (kBM + BN) * kBK * 4 + 1024 + 1024 + 4 * 8192;
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES>,
+    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
     configured = true;
   }
-  const int grid = static_cast<int>(std::min<long long>(a.units, sm_count()));
-  cudaError_t e =
-      launch_pdl(conv_sm100_kernel<MODE, BN, STAGES>, grid, kThreads, smem, st, ta, tb, tc, a);
+  const int grid =
+      CM * static_cast<int>(std::min<long long>(a.units, sm_count() / CM));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CM;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CM > 1 ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
   const long long vec = static_cast<long long>(a.M) * (a.Ng / 4);
@@ -700,6 +801,7 @@ struct Call {
 };
 struct Cfg {
   int bn = 0, splits = 0;
+  int cm = 1;  // CTAs per cluster sharing the B tile by multicast (1 or 2; FWD / DGRAD)
 };
 struct KeyHash {
   size_t operator()(const std::array<int, 14>& k) const {
@@ -722,7 +824,7 @@ bool bn_ok(const Call& c, int bn) {
   }
 }
 
-bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb, Prob& a) {
+bool encode(const Call& c, int bn, int cm, CUtensorMap* ta, CUtensorMap* tb, Prob& a) {
   if (c.mode == FWD) {
     bool ok;
     if (a.a_tiled) {
@@ -738,7 +840,7 @@ bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb, Prob& a) {
     const int Kg = a.R * a.S * a.C;
     const cuuint64_t bd[2] = {static_cast<cuuint64_t>(Kg), static_cast<cuuint64_t>(a.K)};
     const cuuint64_t bs[1] = {static_cast<cuuint64_t>(Kg) * 4};
-    const cuuint32_t bbox[2] = {32, static_cast<cuuint32_t>(bn)};
+    const cuuint32_t bbox[2] = {32, static_cast<cuuint32_t>(bn / cm)};  // cm: half per CTA
     return ok && tiled_map(tb, c.B, 2, bd, bs, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (c.mode == DGRAD) {
@@ -762,7 +864,7 @@ bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb, Prob& a) {
                                 static_cast<cuuint64_t>(a.R) * a.S};
       const cuuint64_t ps[3] = {static_cast<cuuint64_t>(a.C) * a.R * a.S * 4, 128,
                                 static_cast<cuuint64_t>(a.C) * 4};
-      const cuuint32_t pbox[4] = {32, 32, static_cast<cuuint32_t>(bn / 32), 1};
+      const cuuint32_t pbox[4] = {32, 32, static_cast<cuuint32_t>(bn / 32 / cm), 1};
       if (tiled_map(tb, c.B, 4, pd, ps, pbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
         a.b_packed = 1;
         return true;
@@ -808,24 +910,25 @@ bool encode(const Call& c, int bn, CUtensorMap* ta, CUtensorMap* tb, Prob& a) {
                     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int MODE>
+template <int MODE, int CM>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
                 int bn, cudaStream_t st) {
-  if (bn == 256) return launch_t<MODE, 256, 4>(ta, tb, tc, a, st);
-  if (bn == 128) return launch_t<MODE, 128, 6>(ta, tb, tc, a, st);
-  return launch_t<MODE, 64, 8>(ta, tb, tc, a, st);
+  if (bn == 256) return launch_t<MODE, 256, 4, CM>(ta, tb, tc, a, st);
+  if (bn == 128) return launch_t<MODE, 128, 6, CM>(ta, tb, tc, a, st);
+  return launch_t<MODE, 64, 8, CM>(ta, tb, tc, a, st);
 }
 
 // -1: could not encode the tensor maps (not launched)
 int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   CUtensorMap ta, tb;
   Prob a = c.a;
-  if (!encode(c, cfg.bn, &ta, &tb, a)) return -1;
+  if (c.mode == WGRAD) cfg.cm = 1;  // multicast of B across M-tiles: FWD / DGRAD only
+  if (!encode(c, cfg.bn, cfg.cm, &ta, &tb, a)) return -1;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (a.Ng + cfg.bn - 1) / cfg.bn;
   a.splits = cfg.splits;
   a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
-  a.units = a.tiles_m * a.tiles_n * a.splits;
+  a.units = (cfg.cm > 1 ? (a.tiles_m + 1) / 2 : a.tiles_m) * a.tiles_n * a.splits;
   a.ws = g_ws.ws;
   a.trace = g_trace;
   // output tensor map for the bulk-store epilogue: the split-K workspace
@@ -847,9 +950,13 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
     const cuuint32_t box[2] = {32, 32};
     a.tma_out = tiled_map(&tc, a.out, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
   }
-  if (c.mode == FWD) return dispatch_bn<FWD>(ta, tb, tc, a, cfg.bn, st);
-  if (c.mode == DGRAD) return dispatch_bn<DGRAD>(ta, tb, tc, a, cfg.bn, st);
-  return dispatch_bn<WGRAD>(ta, tb, tc, a, cfg.bn, st);
+  if (c.mode == FWD)
+    return cfg.cm > 1 ? dispatch_bn<FWD, 2>(ta, tb, tc, a, cfg.bn, st)
+                      : dispatch_bn<FWD, 1>(ta, tb, tc, a, cfg.bn, st);
+  if (c.mode == DGRAD)
+    return cfg.cm > 1 ? dispatch_bn<DGRAD, 2>(ta, tb, tc, a, cfg.bn, st)
+                      : dispatch_bn<DGRAD, 1>(ta, tb, tc, a, cfg.bn, st);
+  return dispatch_bn<WGRAD, 1>(ta, tb, tc, a, cfg.bn, st);
 }
 
 bool splits_ok(const Call& c, int s) {
@@ -885,11 +992,13 @@ Cfg tune(const Call& c, cudaStream_t st) {
   cudaEventCreate(&e1);
   Cfg best = model_cfg(c);
   float best_ms = 1e30f;
-  for (int bn : {64, 128, 256}) {
+  for (int cm : {1, 2}) {
+   if (cm > 1 && c.mode == WGRAD) continue;
+   for (int bn : {64, 128, 256}) {
     if (!bn_ok(c, bn)) continue;
     for (int s : kSplits) {
       if (!splits_ok(c, s)) continue;
-      const Cfg cand{bn, s};
+      const Cfg cand{bn, s, cm};
       if (launch_cfg(c, cand, st) != 0) {
         cudaGetLastError();
         continue;
@@ -909,13 +1018,23 @@ Cfg tune(const Call& c, cudaStream_t st) {
         best = cand;
       }
     }
+   }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return best;
 }
 
+Cfg g_force{0, 0, 0};  // test hook (accudnn_conv_force_cfg): fields > 0 override
+
 int run_call(const Call& c, cudaStream_t st) {
+  if (g_force.bn > 0 || g_force.splits > 0 || g_force.cm > 0) {
+    Cfg f = model_cfg(c);
+    if (g_force.bn > 0 && bn_ok(c, g_force.bn)) f.bn = g_force.bn;
+    if (g_force.splits > 0 && splits_ok(c, g_force.splits)) f.splits = g_force.splits;
+    if (g_force.cm > 0) f.cm = g_force.cm;
+    return launch_cfg(c, f, st);
+  }
   std::array<int, 14> key;
   std::copy(std::begin(c.key), std::end(c.key), key.begin());
   Cfg cfg;
@@ -1129,7 +1248,8 @@ extern "C" int accudnn_conv_tune_export(char** out) {
   std::string t;
   for (const auto& kv : accudnn::g_tuned) {
     for (int v : kv.first) t += std::to_string(v) + " ";
-    t += std::to_string(kv.second.bn) + " " + std::to_string(kv.second.splits) + "\n";
+    t += std::to_string(kv.second.bn) + " " + std::to_string(kv.second.splits) + " " +
+         std::to_string(kv.second.cm) + "\n";
   }
   char* buf = static_cast<char*>(std::malloc(t.size() + 1));
   if (!buf) return static_cast<int>(cudaErrorMemoryAllocation);
@@ -1150,10 +1270,18 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     for (int& v : key) ok = ok && static_cast<bool>(ls >> v);
     ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
     if (!ok) continue;
+    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2)) cfg.cm = 1;
     if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;
     if (cfg.splits < 1) continue;
     accudnn::g_tuned[key] = cfg;
   }
+  return 0;
+}
+
+// test hook: force (tile width, split-K factor, cluster size) for every TMA
+// conv launch (0 = automatic; an invalid width or split falls back)
+extern "C" int accudnn_conv_force_cfg(int bn, int splits, int cm) {
+  accudnn::g_force = accudnn::Cfg{bn, splits, cm};
   return 0;
 }
 

@@ -63,11 +63,19 @@ def check(got, ref):
     assert (got - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-6
 
 
-@pytest.fixture(params=[1, 0], ids=["tma", "cpasync"])
+@pytest.fixture(params=["tma", "tma_cluster2", "tma_bn64_split3", "cpasync"])
 def impl(request):
+    """TMA kernel with the analytic config, with the B tile multicast across an
+    M-tile pair (cluster of 2), with narrow tiles + forced split-K, and the
+    cp.async kernel."""
     lib = _native.cuda_lib()
-    lib.accudnn_set_conv_impl(request.param)
+    lib.accudnn_set_conv_impl(0 if request.param == "cpasync" else 1)
+    if request.param == "tma_cluster2":
+        lib.accudnn_conv_force_cfg(0, 0, 2)
+    elif request.param == "tma_bn64_split3":
+        lib.accudnn_conv_force_cfg(64, 3, 1)
     yield request.param
+    lib.accudnn_conv_force_cfg(0, 0, 0)
     lib.accudnn_set_conv_impl(1)
 
 

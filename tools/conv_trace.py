@@ -18,6 +18,8 @@ _tune = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                      "conv_tune.txt")
 if os.path.exists(_tune):
     _native.conv_tune_import(open(_tune).read())
+if os.environ.get("ACCUDNN_FORCE"):
+    lib.accudnn_conv_force_cfg(*[int(v) for v in os.environ["ACCUDNN_FORCE"].split(",")])
 p = (h + 2 * pad - r) // st + 1
 q = (w + 2 * pad - r) // st + 1
 d = _native.ConvDesc(n, h, w, c, k, r, r, st, pad, p, q)
