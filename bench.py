@@ -355,10 +355,20 @@ def run_ours(args):
     if os.path.exists(pp):
         peaks = json.load(open(pp))
     bf16 = float(peaks.get("bf16_tflops_sustained", 1405.3))
-    tf32_peak = round(bf16 / 2.0, 1)
+    # the convolutions run TF32: the denominator is the measured sustained
+    # cuBLAS TF32 GEMM rate on this pool's B200s (profiles/b200/tf32_peak.json,
+    # tools/measure_tf32_peak.py); fallback 1/2 of the measured bf16 figure
+    tf32_path = os.path.join(ROOT, "profiles", "b200", "tf32_peak.json")
+    if os.path.exists(tf32_path):
+        tf32_peak = float(json.load(open(tf32_path))["tf32_tflops_sustained"])
+        peak_note = ("measured sustained cuBLAS TF32 GEMM 8192^3 on B200 (profiles/b200/"
+                     "tf32_peak.json); 1/2 of MEASURED_PEAKS bf16 sustained would be %.1f" % (bf16 / 2))
+    else:
+        tf32_peak = round(bf16 / 2.0, 1)
+        peak_note = ("TF32 dense peak taken as 1/2 of the measured cuBLAS bf16 sustained "
+                     "figure in MEASURED_PEAKS.json (nominal 1.1 vs 2.25 PF)")
     roof = roofline_from_trace(desc, trace, k, tf32_peak, len(desc["ops"]))
-    roof["peak_note"] = ("TF32 dense peak taken as 1/2 of the measured cuBLAS bf16 sustained "
-                         "figure in MEASURED_PEAKS.json (nominal 1.1 vs 2.25 PF)")
+    roof["peak_note"] = peak_note
     # DRAM traffic of the conv kernels per launch, from the committed ncu
     # launch list of the same step (profiles/r01, dram__bytes_read+write)
     ls_path = os.path.join(ROOT, "profiles", "r01", f"launch_summary_k{k}.json")
