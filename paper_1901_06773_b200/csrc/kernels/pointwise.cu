@@ -87,6 +87,7 @@ struct BnArgs {
   const float* skip;     // SKIP: y = relu(bn(x) + skip); backward mask uses it too
   float* dskip;          // SKIP, mode 1: gradient of the shortcut (+= when dskip_beta)
   int dskip_beta;
+  int mask_smem;         // SKIP backward launched with the mask buffer (dynamic smem)
   BnWs w;
   long long* trace;      // debug: globaltimer stamps per block (accudnn_bn_trace)
 };
@@ -143,6 +144,16 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   const long long r_begin = blockIdx.y * rows_per_block;
   const long long r_end = min(a.M, r_begin + rows_per_block);
   const long long C = a.C;
+  // SKIP backward: the ReLU mask of each (row, 4 channels) computed in phase 1
+  // is kept as 4 bits in shared memory (kMaskWords words per thread,
+  // thread-interleaved), so phase 3 need not re-read the shortcut tensor
+  extern __shared__ uint32_t mask_smem[];
+  constexpr int kMaskWords = 16;  // 128 rows per thread
+  const long long first_row = r_begin + lane_r;
+  const bool use_mask = MODE == 1 && SKIP && a.mask_smem &&
+                        (rows_per_block + rows_per_pass - 1) / rows_per_pass <= 8 * kMaskWords;
+  if (use_mask)
+    for (int w = 0; w < kMaskWords; ++w) mask_smem[w * kBnThreads + threadIdx.x] = 0u;
 
   // ---- phase 1: per-block partial sums ----
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
@@ -158,9 +169,10 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       fsh[j] = a.beta[c + j] - mu[j] * fsc[j];
     }
   }
-  auto consume = [&](const float4 v, const float4 d, const float4 sk4) {
+  auto consume = [&](const float4 v, const float4 d, const float4 sk4) -> uint32_t {
     const float xv[4] = {v.x, v.y, v.z, v.w};
     const float sk[4] = {sk4.x, sk4.y, sk4.z, sk4.w};
+    uint32_t bits = 0;
     if (MODE == 0) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -174,16 +186,25 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
         const float xh = (xv[j] - mu[j]) * is[j];
         float g = dv[j];
         // the forward's pre-activation, bit for bit (scale/shift as in phase 2 of mode 0)
-        if (a.relu && (xv[j] * fsc[j] + fsh[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
+        if (a.relu && (xv[j] * fsc[j] + fsh[j] + (SKIP ? sk[j] : 0.f)) <= 0.f)
+          g = 0.f;
+        else
+          bits |= 1u << j;
         a0[j] += g;
         a1[j] += g * xh;
       }
     }
+    return bits;
+  };
+  auto keep_mask = [&](int kk, uint32_t bits) {  // kk: row index in this thread's sequence
+    if (!use_mask) return;
+    mask_smem[(kk >> 3) * kBnThreads + threadIdx.x] |= bits << ((kk & 7) * 4);
   };
   const long long step = rows_per_pass;
   if (c_ok) {
     long long r = r_begin + lane_r;
-    for (; r + 3 * step < r_end; r += 4 * step) {  // 4 rows in flight
+    int kk = 0;
+    for (; r + 3 * step < r_end; r += 4 * step, kk += 4) {  // 4 rows in flight
       float4 v[4], d[4], sk[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -194,14 +215,15 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        consume(v[u], MODE == 1 ? d[u] : v[u], (MODE == 1 && SKIP) ? sk[u] : v[u]);
+        keep_mask(kk + u,
+                  consume(v[u], MODE == 1 ? d[u] : v[u], (MODE == 1 && SKIP) ? sk[u] : v[u]));
     }
-    for (; r < r_end; r += step) {
+    for (; r < r_end; r += step, ++kk) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
       const float4 d = MODE == 1 ? __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)) : v;
       const float4 sk =
           (MODE == 1 && SKIP) ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v;
-      consume(v, d, sk);
+      keep_mask(kk, consume(v, d, sk));
     }
   }
   BN_STAMP(1);
@@ -404,16 +426,22 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       mgx[j] = coef[1][cl + j];
       k0[j] = ga[j] * is[j];
     }
-    auto f = [&](const float4 xv4, const float4 dv4, const float4 k4, long long r) {
+    auto f = [&](const float4 xv4, const float4 dv4, const float4 k4, long long r, int kk) {
       const float xv[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
       const float dv[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
       const float sk[4] = {k4.x, k4.y, k4.z, k4.w};
+      uint32_t mbits = 0;
+      if (use_mask) mbits = mask_smem[(kk >> 3) * kBnThreads + threadIdx.x] >> ((kk & 7) * 4);
       float o[4], gg[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float xh = (xv[j] - mu[j]) * is[j];
         float g = dv[j];
-        if (a.relu && (xv[j] * fsc[j] + fsh[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) g = 0.f;
+        if (use_mask) {
+          if (!(mbits >> j & 1u)) g = 0.f;
+        } else if (a.relu && (xv[j] * fsc[j] + fsh[j] + (SKIP ? sk[j] : 0.f)) <= 0.f) {
+          g = 0.f;
+        }
         gg[j] = g;
         o[j] = k0[j] * (g - mg[j] - xh * mgx[j]);
       }
@@ -433,21 +461,25 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       if (SKIP) put(a.dskip, gg, a.dskip_beta);  // d(shortcut) = masked dy
     };
     long long r = r_hi;  // reverse order, as above
-    for (; r - 3 * step >= r_begin; r -= 4 * step) {
+    int kk = static_cast<int>((r_hi - first_row) / step);
+    for (; r - 3 * step >= r_begin; r -= 4 * step, kk -= 4) {
       float4 xv[4], dv[4], kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         xv[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r - u * step) * C + c));
         dv[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r - u * step) * C + c));
-        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r - u * step) * C + c)) : xv[u];
+        kv[u] = (SKIP && !use_mask)
+                    ? __ldg(reinterpret_cast<const float4*>(a.skip + (r - u * step) * C + c))
+                    : xv[u];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], kv[u], r - u * step);
+      for (int u = 0; u < 4; ++u) f(xv[u], dv[u], kv[u], r - u * step, kk - u);
     }
-    for (; r >= r_begin; r -= step) {
+    for (; r >= r_begin; r -= step, --kk) {
       const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
       f(xv, __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)),
-        SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : xv, r);
+        (SKIP && !use_mask) ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : xv, r,
+        kk);
     }
     BN_STAMP(4);
   }
@@ -464,8 +496,11 @@ template <int MODE, bool SKIP>
 int bn_launch(BnArgs a, cudaStream_t st) {
   static int occ = 0;
   if (!occ) {
+    if (MODE == 1 && SKIP)
+      cudaFuncSetAttribute(bn_fused_kernel<MODE, false, SKIP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<MODE, false, SKIP>,
-                                                  kBnThreads, 0);
+                                                  kBnThreads, (MODE == 1 && SKIP) ? 32768 : 0);
     if (occ < 1) occ = 1;
     cudaFuncSetAttribute(bn_fused_kernel<MODE, true, SKIP>,
                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -486,6 +521,18 @@ int bn_launch(BnArgs a, cudaStream_t st) {
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  if (MODE == 1 && SKIP) {  // 32 KB of ReLU-mask bits (see bn_fused_kernel)
+    static bool mask_attr = false;
+    if (!mask_attr) {
+      cudaFuncSetAttribute(bn_fused_kernel<MODE, false, SKIP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
+      cudaFuncSetAttribute(bn_fused_kernel<MODE, true, SKIP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
+      mask_attr = true;
+    }
+    cfg.dynamicSmemBytes = 32768;
+    a.mask_smem = 1;
+  }
   // measured (tools/bn_bench.py, k* = 27 shapes): clusters win for narrow
   // layers with few rows, the cooperative grid for wide or tall ones
   const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);

@@ -1,2 +1,3 @@
-timeout 300 python tools/measure_tf32_peak.py gpurun_out/tf32_peak.json > gpurun_out/tf32.log 2>&1
-nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_event_reasons.active --format=csv >> gpurun_out/tf32.log
+timeout 600 python -m pytest tests/test_layers_gpu.py tests/test_train_step_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+timeout 300 python tools/bn_bench.py 42 > gpurun_out/bn_bench.log 2>&1
