@@ -29,6 +29,12 @@ typedef struct accudnn_conv_desc {
  * beta = 1 accumulates into the output instead of overwriting it. */
 int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, const float* w,
                      float* y, int beta, void* stream);
+/* forward convolution that also writes the batch-norm statistics of its
+ * output: per-32-row column sums and sums of squares, [2][ceil(M/32)][k]
+ * floats (M = n*p*q).  *produced = 0 if the shape ran on the cp.async kernel
+ * (then nothing was written to `stats`). */
+int accudnn_conv_fwd_stats(const accudnn_conv_desc* d, const float* x, const float* w,
+                           float* y, float* stats, int* produced, void* stream);
 int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w,
                        float* dx, int beta, void* stream);
 /* process-wide convolution math: 0 = TF32 tensor cores (default),
@@ -86,6 +92,17 @@ int accudnn_bn_bwd(const float* x, const float* dy, long long M, int C,
  * (training-mode BN over [M][C]); backward recomputes the mask from the
  * inputs and writes both gradients (dx: BN backward, dskip: masked dy;
  * each accumulates when its beta flag is 1). */
+/* the forward batch norms with their statistics precomputed by
+ * accudnn_conv_fwd_stats (only the normalise pass reads x) */
+int accudnn_bn_fwd_stats(const float* x, const float* stats, long long M, int C,
+                         const float* gamma, const float* beta, float eps, int relu, float* y,
+                         float* save_mean, float* save_invstd, float* running_mean,
+                         float* running_var, float momentum, void* ws, void* stream);
+int accudnn_bn_add_relu_fwd_stats(const float* x, const float* stats, const float* skip,
+                                  long long M, int C, const float* gamma, const float* beta,
+                                  float eps, float* y, float* save_mean, float* save_invstd,
+                                  float* running_mean, float* running_var, float momentum,
+                                  void* ws, void* stream);
 int accudnn_bn_add_relu_fwd(const float* x, const float* skip, long long M, int C,
                             const float* gamma, const float* beta, float eps, float* y,
                             float* save_mean, float* save_invstd, float* running_mean,

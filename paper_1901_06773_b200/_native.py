@@ -120,10 +120,14 @@ CUDA_SYMBOLS = {
     "accudnn_bn_trace": ([_P], _I),
     "accudnn_conv_fwd": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
     "accudnn_conv_dgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _P], _I),
+    "accudnn_conv_fwd_stats": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _P, ctypes.POINTER(_I), _P], _I),
     "accudnn_conv_wgrad": ([ctypes.POINTER(ConvDesc), _P, _P, _P, _I, _I, _P], _I),
     "accudnn_bn_workspace_bytes": ([_I], ctypes.c_ulonglong),
     "accudnn_bn_fwd": ([_P, _LL, _I, _P, _P, _F, _I, _P, _P, _P, _P, _P, _F, _P, _P], _I),
     "accudnn_bn_bwd": ([_P, _P, _LL, _I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P, _P], _I),
+    "accudnn_bn_fwd_stats": ([_P, _P, _LL, _I, _P, _P, _F, _I, _P, _P, _P, _P, _P, _F, _P, _P], _I),
+    "accudnn_bn_add_relu_fwd_stats": ([_P, _P, _P, _LL, _I, _P, _P, _F, _P, _P, _P, _P, _P, _F, _P,
+                                       _P], _I),
     "accudnn_bn_add_relu_fwd": ([_P, _P, _LL, _I, _P, _P, _F, _P, _P, _P, _P, _P, _F, _P, _P], _I),
     "accudnn_bn_add_relu_bwd": ([_P, _P, _P, _LL, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P,
                                  _P], _I),

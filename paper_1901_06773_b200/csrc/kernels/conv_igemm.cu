@@ -511,7 +511,7 @@ int sm_count() {
 
 // persistent TMA kernels (conv_sm100.cu); return 0 when a shape is not eligible
 int conv_tma_fwd(const accudnn_conv_desc* d, const float* x, const float* w, float* y, int beta,
-                 cudaStream_t st, int* rc);
+                 cudaStream_t st, int* rc, float* stats = nullptr);
 int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, float* dx,
                    int beta, cudaStream_t st, int* rc);
 int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, float* dw,
@@ -531,6 +531,22 @@ extern "C" int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, cons
   Args a = make_args(d, FWD);
   a.a_src = x; a.b_src = w; a.out = y; a.beta = beta;
   return dispatch<FWD>(a, 1, stream);
+}
+
+// forward that also writes the output's per-32-row column sums / sums of
+// squares ([2][ceil(M/32)][K] floats) for the following batch norm; *produced
+// = 0 when the shape runs on the cp.async kernel (no statistics written)
+extern "C" int accudnn_conv_fwd_stats(const accudnn_conv_desc* d, const float* x, const float* w,
+                                      float* y, float* stats, int* produced, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  *produced = 0;
+  if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
+  int rc = 0;
+  if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_fwd(d, x, w, y, 0, stream, &rc, stats)) {
+    *produced = (rc == 0 && d->k % 32 == 0) ? 1 : 0;  // conv_tma_fwd writes stats iff k % 32 == 0
+    return rc;
+  }
+  return accudnn_conv_fwd(d, x, w, y, 0, stream_);
 }
 
 extern "C" int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w,

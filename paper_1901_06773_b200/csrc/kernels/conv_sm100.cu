@@ -83,6 +83,8 @@ struct Prob {
   float* ws;           // split-K partials [split][M][Ng]
   long long* trace;    // debug: per-CTA clock64 stamps (accudnn_conv_trace), or nullptr
   int tma_out;         // epilogue stores through tmC (bulk tensor stores / reduce-adds)
+  float* stats;        // FWD: per-32-row column sums / sums of squares [2][ceil(M/32)][Ng]
+                       // of the output (the next batch norm's statistics), or nullptr
   int a_packed;        // WGRAD: A stage (4 MN atoms) is one 3-D TMA box
   int b_packed;        // DGRAD: B stage (BN/32 MN atoms) is one 4-D box; WGRAD 1x1: one 3-D box
 };
@@ -492,6 +494,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                            sbuf + lane * 128 + ((g ^ (lane & 7)) << 4)),
                        "f"(cur[4 * g]), "f"(cur[4 * g + 1]), "f"(cur[4 * g + 2]), "f"(cur[4 * g + 3])
                        : "memory");
+        if (a.stats && !partial) {
+          // column sums of this 32x32 chunk for the next batch norm: lane l
+          // walks column l of the staged (swizzled) chunk; rows past M skipped
+          __syncwarp();
+          const int col = n0 + c0 + lane;
+          float cs = 0.f, cq = 0.f;
+          const int nrows = min(32, a.M - m0);
+#pragma unroll 8
+          for (int r = 0; r < nrows; ++r) {
+            float v;
+            asm volatile("ld.shared.f32 %0, [%1];"
+                         : "=f"(v)
+                         : "r"(sbuf + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4));
+            cs += v;
+            cq += v * v;
+          }
+          if (nrows > 0 && col < a.Ng) {
+            const long long P = (a.M + 31) / 32;
+            const long long slot = m0 / 32;
+            a.stats[slot * a.Ng + col] = cs;
+            a.stats[(P + slot) * a.Ng + col] = cq;
+          }
+        }
         if (a.tma_out) {
           fence_async_smem();
           __syncwarp();
@@ -596,6 +621,60 @@ __global__ void __launch_bounds__(256) conv_splitk_reduce_kernel(const Prob a) {
       o.w += old.w;
     }
     *d = o;
+  }
+}
+
+// split-K reduction that also produces the batch-norm column statistics of
+// the output.  Block = 32 rows x 32 columns (thread = row x float4): slices
+// summed in order per element, then the column sums over the 32 rows in a
+// fixed smem order -> one [2][P][Ng] partial slot per (32-row block, column).
+__global__ void __launch_bounds__(256) conv_splitk_reduce_stats_kernel(const Prob a) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float4 red1[32][8], red2[32][8];
+  const int cbs = a.Ng / 32;
+  const long long P = (a.M + 31) / 32;
+  const long long slice = static_cast<long long>(a.M) * a.Ng;
+  const int tr = threadIdx.x >> 3, tc = threadIdx.x & 7;
+  for (long long blk = blockIdx.x; blk < P * cbs; blk += gridDim.x) {
+    const long long pb = blk / cbs;
+    const int c = static_cast<int>(blk - pb * cbs) * 32 + tc * 4;
+    const long long m = pb * 32 + tr;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (m < a.M) {
+      const float* src = a.ws + m * a.Ng + c;
+      o = __ldcg(reinterpret_cast<const float4*>(src));
+      for (int s0 = 1; s0 < a.splits; s0 += 8) {
+        float4 p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < a.splits) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + u) * slice));
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < a.splits) {
+            o.x += p[u].x;
+            o.y += p[u].y;
+            o.z += p[u].z;
+            o.w += p[u].w;
+          }
+      }
+      *reinterpret_cast<float4*>(a.out + m * a.Ng + c) = o;
+    }
+    red1[tr][tc] = o;
+    red2[tr][tc] = make_float4(o.x * o.x, o.y * o.y, o.z * o.z, o.w * o.w);
+    __syncthreads();
+    if (threadIdx.x < 8) {  // column group tc = threadIdx.x, rows in order
+      float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s1;
+      for (int r = 0; r < 32; ++r) {
+        const float4 u = red1[r][threadIdx.x], v = red2[r][threadIdx.x];
+        s1.x += u.x; s1.y += u.y; s1.z += u.z; s1.w += u.w;
+        s2.x += v.x; s2.y += v.y; s2.z += v.z; s2.w += v.w;
+      }
+      const int cc = static_cast<int>(blk - pb * cbs) * 32 + threadIdx.x * 4;
+      *reinterpret_cast<float4*>(a.stats + pb * a.Ng + cc) = s1;
+      *reinterpret_cast<float4*>(a.stats + (P + pb) * a.Ng + cc) = s2;
+    }
+    __syncthreads();
   }
 }
 
@@ -754,6 +833,12 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   cudaError_t e = cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
+  if (a.stats) {
+    const long long blocks = (static_cast<long long>(a.M) + 31) / 32 * (a.Ng / 32);
+    const int rgrid = static_cast<int>(std::min<long long>(blocks, 16LL * sm_count()));
+    launch_pdl(conv_splitk_reduce_stats_kernel, rgrid, 256, 0, st, a);
+    return static_cast<int>(cudaGetLastError());
+  }
   const long long vec = static_cast<long long>(a.M) * (a.Ng / 4);
   const int rgrid = static_cast<int>(std::min<long long>((vec + 255) / 256, 8LL * sm_count()));
   launch_pdl(conv_splitk_reduce_kernel, rgrid, 256, 0, st, a);
@@ -1084,7 +1169,7 @@ void fill_key(Call& c, const accudnn_conv_desc* d, int cls) {
 
 // 0 = not eligible (caller falls back to the cp.async kernel), else launched
 int conv_tma_fwd(const accudnn_conv_desc* d, const float* x, const float* w, float* y, int beta,
-                 cudaStream_t st, int* rc) {
+                 cudaStream_t st, int* rc, float* stats) {
   if (!geometry_ok(d) || (d->c % 32) || (d->k % 4)) return 0;
   Call c;
   c.mode = FWD;
@@ -1095,6 +1180,7 @@ int conv_tma_fwd(const accudnn_conv_desc* d, const float* x, const float* w, flo
   a.kb_total = a.R * a.S * a.C / kBK;
   a.out = y;
   a.beta = beta;
+  a.stats = (beta || a.K % 32) ? nullptr : stats;
   a.a_tiled = (a.R == 1 && a.stride == 1 && a.pad == 0);
   c.A = x;
   c.B = w;

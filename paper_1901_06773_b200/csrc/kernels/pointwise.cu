@@ -88,6 +88,8 @@ struct BnArgs {
   float* dskip;          // SKIP, mode 1: gradient of the shortcut (+= when dskip_beta)
   int dskip_beta;
   int mask_smem;         // SKIP backward launched with the mask buffer (dynamic smem)
+  const float* stats_in; // mode 0: the producing conv's column sums [2][P][C] (P = ceil(M/32)):
+                         // phase 1 sums these instead of reading x
   BnWs w;
   long long* trace;      // debug: globaltimer stamps per block (accudnn_bn_trace)
 };
@@ -201,7 +203,26 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     mask_smem[(kk >> 3) * kBnThreads + threadIdx.x] |= bits << ((kk & 7) * 4);
   };
   const long long step = rows_per_pass;
-  if (c_ok) {
+  if (MODE == 0 && a.stats_in) {
+    // statistics precomputed by the conv epilogue: sum this block's share
+    // of the 32-row partial slots (same fixed order as every other block)
+    const long long P = (a.M + 31) / 32;
+    const long long sp = (P + a.Y - 1) / a.Y;
+    const long long s0 = blockIdx.y * sp, s1 = min(P, s0 + sp);
+    if (c_ok)
+      for (long long r = s0 + lane_r; r < s1; r += step) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.stats_in + r * C + c));
+        const float4 q = __ldcg(reinterpret_cast<const float4*>(a.stats_in + (P + r) * C + c));
+        a0[0] += v.x;
+        a0[1] += v.y;
+        a0[2] += v.z;
+        a0[3] += v.w;
+        a1[0] += q.x;
+        a1[1] += q.y;
+        a1[2] += q.z;
+        a1[3] += q.w;
+      }
+  } else if (c_ok) {
     long long r = r_begin + lane_r;
     int kk = 0;
     for (; r + 3 * step < r_end; r += 4 * step, kk += 4) {  // 4 rows in flight
@@ -1006,6 +1027,35 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
   return bn_launch<0, false>(a, S(stream));
 }
 
+// forward batch norm whose statistics come from the producing convolution
+// (accudnn_conv_fwd_stats): only the normalise pass reads x
+extern "C" int accudnn_bn_fwd_stats(const float* x, const float* stats, long long M, int C,
+                                    const float* gamma, const float* beta, float eps, int relu,
+                                    float* y, float* save_mean, float* save_invstd,
+                                    float* running_mean, float* running_var, float momentum,
+                                    void* ws, void* stream) {
+  if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups || !stats)
+    return static_cast<int>(cudaErrorInvalidValue);
+  BnArgs a{};
+  a.x = x;
+  a.stats_in = stats;
+  a.M = M;
+  a.C = C;
+  a.relu = relu;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.eps = eps;
+  a.momentum = momentum;
+  a.save_mean = save_mean;
+  a.save_invstd = save_invstd;
+  a.run_mean = running_mean;
+  a.run_var = running_var;
+  a.y = y;
+  a.w = bn_ws(ws, C);
+  a.trace = g_bn_trace;
+  return bn_launch<0, false>(a, S(stream));
+}
+
 extern "C" int accudnn_bn_bwd(const float* x, const float* dy, long long M, int C,
                               const float* gamma, const float* beta, const float* save_mean,
                               const float* save_invstd, int relu, float* dx, int dx_beta,
@@ -1039,6 +1089,34 @@ extern "C" int accudnn_bn_add_relu_fwd(const float* x, const float* skip, long l
   if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups) return static_cast<int>(cudaErrorInvalidValue);
   BnArgs a{};
   a.x = x;
+  a.skip = skip;
+  a.M = M;
+  a.C = C;
+  a.relu = 1;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.eps = eps;
+  a.momentum = momentum;
+  a.save_mean = save_mean;
+  a.save_invstd = save_invstd;
+  a.run_mean = running_mean;
+  a.run_var = running_var;
+  a.y = y;
+  a.w = bn_ws(ws, C);
+  return bn_launch<0, true>(a, S(stream));
+}
+
+extern "C" int accudnn_bn_add_relu_fwd_stats(const float* x, const float* stats,
+                                             const float* skip, long long M, int C,
+                                             const float* gamma, const float* beta, float eps,
+                                             float* y, float* save_mean, float* save_invstd,
+                                             float* running_mean, float* running_var,
+                                             float momentum, void* ws, void* stream) {
+  if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups || !stats)
+    return static_cast<int>(cudaErrorInvalidValue);
+  BnArgs a{};
+  a.x = x;
+  a.stats_in = stats;
   a.skip = skip;
   a.M = M;
   a.C = C;

@@ -48,6 +48,12 @@ struct Executor::Impl {
   float* loss = nullptr;
   float* loss_host = nullptr;    // pinned
   void* conv_ws = nullptr;       // split-K partials of the conv kernels
+  // batch-norm statistics written by the producing convolution (two slots:
+  // conv o uses slot o % 2, read by its BN consumer before the slot is reused)
+  float* bn_stats[2] = {nullptr, nullptr};
+  size_t bn_stats_bytes = 0;
+  std::vector<char> stats_from_conv;  // op -> its BN input's statistics are in a slot
+  std::vector<char> stats_ok;         // op -> may produce statistics (slot not reused early)
   std::vector<float*> host_store;  // pinned host copies of swapped featuremaps
   // streams / events
   cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr, comm_stream = nullptr;
@@ -121,6 +127,22 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   const size_t img4 = sizeof(float) * static_cast<size_t>(k) * cfg.image * cfg.image * net_.in_c4;
   const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg.image * cfg.image * net_.in_c;
   fixed_bytes_ = 3 * pbytes + sbytes + wsbytes + img4 + img3 + sizeof(int) * k + 256;
+  // conv-produced BN statistics: [2][ceil(M/32)][C] floats per slot
+  {
+    size_t need = 0;
+    for (int o = 0; o < n; ++o) {
+      const Op& op = net_.ops[static_cast<size_t>(o)];
+      if (op.kind != OpKind::conv) continue;
+      const auto& cons = net_.consumers[static_cast<size_t>(o)];
+      if (cons.size() != 1 || !is_bn(net_.ops[static_cast<size_t>(cons[0])].kind)) continue;
+      const TensorShape& so = net_.shape[static_cast<size_t>(o)];
+      const long long M = static_cast<long long>(k) * so.h * so.w;
+      need = std::max(need, sizeof(float) * 2 * static_cast<size_t>((M + 31) / 32) * so.c);
+    }
+    if (!cfg.conv_bn_stats) need = 0;
+    I.bn_stats_bytes = need;
+    fixed_bytes_ += 2 * need;
+  }
   // split-K workspace of the convolutions: whatever the planner's fixed
   // allowance leaves, capped at 64 MiB; the kernels pick their split
   // factors to fit it
@@ -155,6 +177,26 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaMalloc(&I.loss, 256), "loss");
   ck(cudaMallocHost(&I.loss_host, sizeof(float)), "loss host");
   if (conv_ws) ck(cudaMalloc(&I.conv_ws, conv_ws), "conv workspace");
+  if (I.bn_stats_bytes)
+    for (auto& p : I.bn_stats) ck(cudaMalloc(&p, I.bn_stats_bytes), "bn stats");
+  I.stats_from_conv.assign(static_cast<size_t>(n), 0);
+  // a conv may hand its statistics to its BN consumer only if no other
+  // statistics-producing conv of the same slot parity runs in between
+  I.stats_ok.assign(static_cast<size_t>(n), 0);
+  for (int o = 0; o < n; ++o) {
+    const auto& cons = net_.consumers[static_cast<size_t>(o)];
+    if (net_.ops[static_cast<size_t>(o)].kind != OpKind::conv || cons.size() != 1 ||
+        !is_bn(net_.ops[static_cast<size_t>(cons[0])].kind))
+      continue;
+    bool ok = true;
+    for (int q = o + 1; q < cons[0]; ++q) {
+      const auto& cq = net_.consumers[static_cast<size_t>(q)];
+      if (net_.ops[static_cast<size_t>(q)].kind == OpKind::conv && q % 2 == o % 2 &&
+          cq.size() == 1 && is_bn(net_.ops[static_cast<size_t>(cq[0])].kind))
+        ok = false;
+    }
+    I.stats_ok[static_cast<size_t>(o)] = ok;
+  }
   ckl(accudnn_conv_set_workspace(I.conv_ws, I.conv_ws ? conv_ws : 0), "conv workspace");
   if (cfg.autotune) accudnn_conv_autotune(1);
   ck(cudaMemset(I.params, 0, pbytes), "memset");
@@ -219,7 +261,8 @@ Executor::~Executor() {
                   static_cast<void*>(I.grads), static_cast<void*>(I.momentum_buf),
                   static_cast<void*>(I.stats), I.bn_ws, static_cast<void*>(I.image),
                   static_cast<void*>(I.image_nchw), static_cast<void*>(I.labels),
-                  static_cast<void*>(I.loss), I.conv_ws})
+                  static_cast<void*>(I.loss), I.conv_ws, static_cast<void*>(I.bn_stats[0]),
+                  static_cast<void*>(I.bn_stats[1])})
     if (p) cudaFree(p);
   if (I.conv_ws || cfg_.budget) accudnn_conv_set_workspace(nullptr, 64ull << 20);
 }
@@ -300,7 +343,17 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     switch (op.kind) {
       case OpKind::conv: {
         const accudnn_conv_desc d = conv_desc(op);
-        ckl(accudnn_conv_fwd(&d, act(op.in0, s), I.params + op.w_off, y, 0, csv), "conv fwd");
+        const auto& cons = net.consumers[static_cast<size_t>(o)];
+        I.stats_from_conv[static_cast<size_t>(o)] = 0;
+        if (I.bn_stats_bytes && I.stats_ok[static_cast<size_t>(o)]) {
+          int produced = 0;
+          ckl(accudnn_conv_fwd_stats(&d, act(op.in0, s), I.params + op.w_off, y,
+                                     I.bn_stats[o % 2], &produced, csv),
+              "conv fwd");
+          I.stats_from_conv[static_cast<size_t>(o)] = static_cast<char>(produced);
+        } else {
+          ckl(accudnn_conv_fwd(&d, act(op.in0, s), I.params + op.w_off, y, 0, csv), "conv fwd");
+        }
         break;
       }
       case OpKind::fc: {
@@ -313,20 +366,35 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       case OpKind::bn_relu: {
         const int C = op.channels;
         float* sp = I.stats + op.stat_off;
-        ckl(accudnn_bn_fwd(act(op.in0, s), elems(o) / C, C, I.params + op.g_off,
-                           I.params + op.beta_off, cfg_.bn_eps, op.kind == OpKind::bn_relu, y,
-                           sp, sp + C, sp + 2 * C, sp + 3 * C, cfg_.bn_momentum, I.bn_ws, csv),
-            "bn fwd");
+        if (op.in0 >= 0 && I.stats_from_conv[static_cast<size_t>(op.in0)])
+          ckl(accudnn_bn_fwd_stats(act(op.in0, s), I.bn_stats[op.in0 % 2], elems(o) / C, C,
+                                   I.params + op.g_off, I.params + op.beta_off, cfg_.bn_eps,
+                                   op.kind == OpKind::bn_relu, y, sp, sp + C, sp + 2 * C,
+                                   sp + 3 * C, cfg_.bn_momentum, I.bn_ws, csv),
+              "bn fwd");
+        else
+          ckl(accudnn_bn_fwd(act(op.in0, s), elems(o) / C, C, I.params + op.g_off,
+                             I.params + op.beta_off, cfg_.bn_eps, op.kind == OpKind::bn_relu, y,
+                             sp, sp + C, sp + 2 * C, sp + 3 * C, cfg_.bn_momentum, I.bn_ws, csv),
+              "bn fwd");
         break;
       }
       case OpKind::bn_add_relu: {
         const int C = op.channels;
         float* sp = I.stats + op.stat_off;
-        ckl(accudnn_bn_add_relu_fwd(act(op.in0, s), act(op.in1, s), elems(o) / C, C,
-                                    I.params + op.g_off, I.params + op.beta_off, cfg_.bn_eps, y,
-                                    sp, sp + C, sp + 2 * C, sp + 3 * C, cfg_.bn_momentum, I.bn_ws,
-                                    csv),
-            "bn_add_relu fwd");
+        if (op.in0 >= 0 && I.stats_from_conv[static_cast<size_t>(op.in0)])
+          ckl(accudnn_bn_add_relu_fwd_stats(act(op.in0, s), I.bn_stats[op.in0 % 2],
+                                            act(op.in1, s), elems(o) / C, C, I.params + op.g_off,
+                                            I.params + op.beta_off, cfg_.bn_eps, y, sp, sp + C,
+                                            sp + 2 * C, sp + 3 * C, cfg_.bn_momentum, I.bn_ws,
+                                            csv),
+              "bn_add_relu fwd");
+        else
+          ckl(accudnn_bn_add_relu_fwd(act(op.in0, s), act(op.in1, s), elems(o) / C, C,
+                                      I.params + op.g_off, I.params + op.beta_off, cfg_.bn_eps, y,
+                                      sp, sp + C, sp + 2 * C, sp + 3 * C, cfg_.bn_momentum,
+                                      I.bn_ws, csv),
+              "bn_add_relu fwd");
         break;
       }
       case OpKind::relu:

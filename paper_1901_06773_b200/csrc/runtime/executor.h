@@ -43,6 +43,11 @@ struct ExecConfig {
   int device = 0;
   long long bucket_bytes = 25LL << 20;
   int autotune = 1;                // tune conv tile/split-K per shape in the first (eager) step
+  // batch-norm statistics from the producing conv's epilogue
+  // (accudnn_conv_fwd_stats + accudnn_bn_*_fwd_stats).  Measured on ResNet-152
+  // k*=42: 2218 vs 2243 img/s -- the epilogue cost exceeds the saved read --
+  // so off by default.
+  int conv_bn_stats = 0;
 };
 
 struct StepStats {

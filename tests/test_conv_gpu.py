@@ -206,3 +206,59 @@ def test_dgrad_strided_accumulate(cuda_dev, shape):
     torch.cuda.synchronize()
     assert not torch.isnan(fresh).any()
     assert torch.allclose(acc, base + fresh, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("shape,forced", [((8, 256, 14, 14, 1024, 1, 1, 0), (0, 0, 0)),
+                                          ((27, 1024, 14, 14, 256, 1, 1, 0), (256, 4, 1)),
+                                          ((4, 64, 28, 28, 64, 3, 1, 1), (0, 0, 2)),
+                                          ((3, 96, 10, 10, 160, 3, 1, 1), (0, 0, 0))])
+def test_conv_fwd_stats_and_bn_from_stats(cuda_dev, shape, forced):
+    """the forward conv's epilogue (or its split-K reduce) writes per-32-row
+    column sums / sums of squares of the output; a batch norm fed with them
+    equals the one that reads the output itself"""
+    lib = _native.cuda_lib()
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    lib.accudnn_conv_force_cfg(*forced)
+    try:
+        x = torch.randn(n, h, w, c, device=cuda_dev)
+        wt = torch.randn(k, r, r, c, device=cuda_dev) * (1.0 / (c * r * r) ** 0.5)
+        y = torch.empty(n, p, q, k, device=cuda_dev)
+        M = n * p * q
+        P = (M + 31) // 32
+        stats = torch.full((2, P, k), float("nan"), device=cuda_dev)
+        produced = ctypes.c_int(0)
+        assert lib.accudnn_conv_fwd_stats(ctypes.byref(d), x.data_ptr(), wt.data_ptr(), y.data_ptr(),
+                                          stats.data_ptr(), ctypes.byref(produced), None) == 0
+        torch.cuda.synchronize()
+    finally:
+        lib.accudnn_conv_force_cfg(0, 0, 0)
+    assert produced.value == 1
+    yf = y.reshape(M, k).double()
+    pad_rows = P * 32 - M
+    yp = torch.cat([yf, torch.zeros(pad_rows, k, device=cuda_dev, dtype=torch.float64)])
+    ref1 = yp.reshape(P, 32, k).sum(1)
+    ref2 = (yp * yp).reshape(P, 32, k).sum(1)
+    assert rel_err(stats[0].double(), ref1) < 1e-5
+    assert rel_err(stats[1].double(), ref2) < 1e-5
+    g, b = torch.rand(k, device=cuda_dev) + 0.5, torch.randn(k, device=cuda_dev) * 0.1
+    ws = torch.zeros(lib.accudnn_bn_workspace_bytes(k) // 4 + 1, device=cuda_dev)
+    P_ = ctypes.c_void_p
+    outs = []
+    for use_stats in (False, True):
+        yy = torch.empty_like(y)
+        mean, inv = torch.empty(k, device=cuda_dev), torch.empty(k, device=cuda_dev)
+        if use_stats:
+            rc = lib.accudnn_bn_fwd_stats(P_(y.data_ptr()), P_(stats.data_ptr()), M, k, P_(g.data_ptr()),
+                                          P_(b.data_ptr()), 1e-5, 1, P_(yy.data_ptr()), P_(mean.data_ptr()),
+                                          P_(inv.data_ptr()), None, None, 0.1, P_(ws.data_ptr()), None)
+        else:
+            rc = lib.accudnn_bn_fwd(P_(y.data_ptr()), M, k, P_(g.data_ptr()), P_(b.data_ptr()), 1e-5, 1,
+                                    P_(yy.data_ptr()), P_(mean.data_ptr()), P_(inv.data_ptr()), None,
+                                    None, 0.1, P_(ws.data_ptr()), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs.append((yy, mean, inv))
+    assert rel_err(outs[1][1].double(), outs[0][1].double()) < 1e-5
+    assert rel_err(outs[1][2].double(), outs[0][2].double()) < 1e-4
+    assert rel_err(outs[1][0].double(), outs[0][0].double()) < 1e-4

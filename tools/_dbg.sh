@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests/test_layers_gpu.py tests/test_train_step_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1
-timeout 300 python tools/bn_bench.py 42 > gpurun_out/bn_bench.log 2>&1
