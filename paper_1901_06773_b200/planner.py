@@ -13,6 +13,7 @@ passing ``lib=`` and ``prefix="oracle_"``.
 
 import ctypes
 import json
+import os
 
 from . import _native
 
@@ -170,3 +171,39 @@ def generate_fixture(seed, min_layers=0, max_layers=0, *, lib=None, prefix="accu
     if rc != 0:
         raise PlannerError(rc, B.error())
     return dict(zip(("network", "hardware", "compute_csv", "transfer_csv"), texts))
+
+
+def _fnv1a(chunks):
+    h = 1469598103934665603
+    for data in chunks:
+        for c in data:
+            h ^= c
+            h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return "%016x" % h
+
+
+def plan_cached(network_json, hardware_json, model_json, cache_dir, *, step=1, k_override=0,
+                epochs=1, dataset_size=0, budget_override=0, lib=None, prefix="accudnn_"):
+    """plan() behind a persistent cache keyed by the reference's manifest
+    digest of the `plan` run (FNV-1a over the subcommand, the three documents
+    and the `key=value;` parameters, swapsched.cpp:76-91): the same inputs
+    return the stored plan.json without re-planning.  Returns (plan_json, hit)."""
+    params = [("step", step), ("k", k_override), ("epochs", epochs),
+              ("dataset_size", dataset_size)]
+    if budget_override:
+        params.append(("budget", budget_override))
+    digest = _fnv1a([b"plan", _b(network_json), _b(hardware_json), _b(model_json)] +
+                    [f"{k}={v};".encode() for k, v in params])
+    path = os.path.join(cache_dir, f"plan-{digest}.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return f.read(), True
+    text = plan(network_json, hardware_json, model_json, step=step, k_override=k_override,
+                epochs=epochs, dataset_size=dataset_size, budget_override=budget_override,
+                lib=lib, prefix=prefix)
+    os.makedirs(cache_dir, exist_ok=True)
+    tmp = path + ".tmp"
+    with open(tmp, "w") as f:
+        f.write(text)
+    os.replace(tmp, path)
+    return text, False

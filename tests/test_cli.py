@@ -101,3 +101,20 @@ def test_cli_execute_on_gpu(tmp_path, cuda_dev):
     assert s["k"] == 16 and s["iter_time_s"] > 0 and s["peak_device_bytes"] <= 0.25 * (1 << 30)
     rows = open(out / "trace.csv").read().strip().splitlines()
     assert len(rows) == 1 + 2 * json.load(open(net))["num_layers"]
+
+
+def test_plan_cache_keyed_by_manifest_digest(fixture_dir):
+    net, hw, comp, tran = (open(p).read() for p in paths(fixture_dir))
+    model = planner.fit(net, [comp, tran], hw)
+    cache = str(fixture_dir / "cache")
+    p1, hit1 = planner.plan_cached(net, hw, model, cache)
+    p2, hit2 = planner.plan_cached(net, hw, model, cache)
+    assert (hit1, hit2) == (False, True) and p1 == p2 == planner.plan(net, hw, model)
+    p3, hit3 = planner.plan_cached(net, hw, model, cache, k_override=4)
+    assert not hit3 and json.loads(p3)["k_star"] == 4
+    # the key is the manifest digest of a `plan` run on files with these bytes
+    for name, text in (("n.json", net), ("h.json", hw), ("m.json", model)):
+        (fixture_dir / name).write_text(text)
+    d = cli.manifest_digest("plan", [str(fixture_dir / n) for n in ("n.json", "h.json", "m.json")],
+                            [("step", "1"), ("k", "0"), ("epochs", "1"), ("dataset_size", "0")])
+    assert os.path.exists(os.path.join(cache, f"plan-{d}.json"))
