@@ -339,15 +339,20 @@ def run_ours(args):
     value = world * k / (ms_per_step * 1e-3)
 
     # ---- timed: end to end with pinned host inputs ----
+    # pipelined input (the user-facing data path): every step copies the next
+    # batch H2D from pinned host memory on a side stream while it computes,
+    # and reads the loss back; one batch copy + one loss read per timed step
+    ex.step_pipelined(x_host, y_host, lr=lr, next_images=x_host)  # prime the pipeline
     barrier()
     t0 = time.perf_counter()
     e2e_dev_ms = 0.0
     for _ in range(args.steps):
-        st = ex.step(x_host, y_host, lr=lr)
+        st = ex.step_pipelined(None, y_host, lr=lr, next_images=x_host)
         e2e_dev_ms += st["iter_ms"]
     barrier()
     e2e_wall = max_over_ranks((time.perf_counter() - t0) / args.steps)
     e2e_value = world * k / e2e_wall
+    ex.step(x_dev, y_dev, lr=lr)  # drop the outstanding prefetch before the profiled steps
 
     ours_launches, all_device_ops = count_kernel_launches(lambda: ex.step(x_dev, y_dev, lr=lr))
 

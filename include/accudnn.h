@@ -64,6 +64,13 @@ int accudnn_exec_set_graph(accudnn_exec* ex, int enable);
  * are host pointers (copied inside the step), 0 when device pointers */
 int accudnn_exec_step(accudnn_exec* ex, const float* images, const int* labels, int host_inputs,
                       float lr, int update, int profile, accudnn_step_stats* out);
+/* pipelined host input: images == NULL uses the batch the previous call
+ * prefetched; next_images (host, may be NULL) is copied H2D on a side stream
+ * as soon as this step's input layout kernel has consumed the staging buffer,
+ * overlapping the rest of the step.  Labels are copied inside the step. */
+int accudnn_exec_step_pipelined(accudnn_exec* ex, const float* images, const int* labels,
+                                float lr, int update, const float* next_images,
+                                accudnn_step_stats* out);
 int accudnn_exec_memory(accudnn_exec* ex, unsigned long long* arena_bytes,
                         unsigned long long* fixed_bytes);
 int accudnn_exec_launches(accudnn_exec* ex);

@@ -30,6 +30,7 @@ SYMBOLS = {
     "accudnn_exec_get_stats": ([_P, _P, _LL], _I),
     "accudnn_exec_set_graph": ([_P, _I], _I),
     "accudnn_exec_step": ([_P, _P, _P, _I, _F, _I, _I, ctypes.POINTER(StepStats)], _I),
+    "accudnn_exec_step_pipelined": ([_P, _P, _P, _F, _I, _P, ctypes.POINTER(StepStats)], _I),
     "accudnn_exec_memory": ([_P, _ULLP, _ULLP], _I),
     "accudnn_exec_launches": ([_P], _I),
     "accudnn_exec_trace": ([_P, ctypes.POINTER(_P)], _I),

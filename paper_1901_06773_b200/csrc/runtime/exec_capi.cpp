@@ -188,6 +188,23 @@ int accudnn_exec_step(accudnn_exec* ex, const float* images, const int* labels, 
   });
 }
 
+int accudnn_exec_step_pipelined(accudnn_exec* ex, const float* images, const int* labels,
+                                float lr, int update, const float* next_images,
+                                accudnn_step_stats* out) {
+  return guarded([&] {
+    const accudnn::StepStats s = ex->ex->step(images, labels, 1, lr, update, 0, next_images);
+    if (out) {
+      out->loss = s.loss;
+      out->iter_ms = s.iter_ms;
+      out->exposed_swap_ms = s.exposed_swap_ms;
+      out->allreduce_ms = s.allreduce_ms;
+      out->peak_bytes = s.peak_bytes;
+      out->swapped_bytes = s.swapped_bytes;
+    }
+    return 0;
+  });
+}
+
 int accudnn_exec_memory(accudnn_exec* ex, unsigned long long* arena, unsigned long long* fixed) {
   if (arena) *arena = ex->ex->arena_bytes();
   if (fixed) *fixed = ex->ex->fixed_bytes();

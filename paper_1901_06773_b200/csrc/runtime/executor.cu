@@ -57,6 +57,10 @@ struct Executor::Impl {
   std::vector<float*> host_store;  // pinned host copies of swapped featuremaps
   // streams / events
   cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr, comm_stream = nullptr;
+  cudaStream_t input_stream = nullptr;  // pipelined next-batch H2D
+  cudaEvent_t layout_done = nullptr;    // staging buffer consumed (record node in the graph)
+  cudaEvent_t input_ready = nullptr;    // next batch landed in the staging buffer
+  bool prefetched = false;
   std::vector<cudaEvent_t> step_done;   // per step
   std::vector<cudaEvent_t> d2h_done;    // per tensor
   std::vector<cudaEvent_t> h2d_done;    // per tensor
@@ -226,6 +230,9 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaStreamCreateWithFlags(&I.d2h, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.h2d, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.comm_stream, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&I.input_stream, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreateWithFlags(&I.layout_done, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&I.input_ready, cudaEventDisableTiming), "event");
   auto mk = [](std::vector<cudaEvent_t>& v, size_t cnt, bool timing) {
     v.assign(cnt, nullptr);
     for (auto& e : v)
@@ -250,9 +257,9 @@ Executor::~Executor() {
                   &I.bucket_ready})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done})
+  for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done, I.layout_done, I.input_ready})
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {I.compute, I.d2h, I.h2d, I.comm_stream})
+  for (cudaStream_t s : {I.compute, I.d2h, I.h2d, I.comm_stream, I.input_stream})
     if (s) cudaStreamDestroy(s);
   for (float* h : I.host_store)
     if (h) cudaFreeHost(h);
@@ -296,7 +303,7 @@ void Executor::set_comm(const void* uid, int rank, int world) {
 }
 
 StepStats Executor::step(const void* images, const int* labels, int host_inputs, float lr,
-                         int update, int profile) {
+                         int update, int profile, const void* next_images) {
   Impl& I = *impl_;
   const int n = I.n;
   const int k = cfg_.k;
@@ -539,7 +546,8 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     int launches = 0;
     if (host_inputs && !capture) {
       const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
-      ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyHostToDevice, cs), "h2d images");
+      if (images)
+        ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyHostToDevice, cs), "h2d images");
       ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyHostToDevice, cs), "h2d labels");
     }
     const float* src = (host_inputs || capture) ? I.image_nchw : static_cast<const float*>(images);
@@ -547,6 +555,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyDeviceToDevice, cs), "labels");
     ckl(accudnn_nchw_to_nhwc_pad(src, k, net.in_c, cfg_.image, cfg_.image, net.in_c4, I.image, csv),
         "image layout");
+    // the staging buffer is free from here on: the next batch may land in it
+    ck(cudaEventRecordWithFlags(I.layout_done, cs, capture ? cudaEventRecordExternal : 0),
+       "record");
     ++launches;
     long long reduced = 0;
     const long long bucket = std::max<long long>(1, cfg_.bucket_bytes / 4);
@@ -650,12 +661,19 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     return launches;
   };
 
+  if (!images) {
+    if (!host_inputs || !I.prefetched)
+      throw std::invalid_argument("step without images needs a batch prefetched by the previous step");
+    ck(cudaStreamWaitEvent(cs, I.input_ready, 0), "wait input");
+    I.prefetched = false;
+  }
   ck(cudaEventRecord(I.iter_begin, cs), "record");
   const bool graph_ok = use_graph && !profile && update && !I.first_step;
   if (graph_ok) {
     if (host_inputs) {
       const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
-      ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyHostToDevice, cs), "h2d images");
+      if (images)
+        ck(cudaMemcpyAsync(I.image_nchw, images, img3, cudaMemcpyHostToDevice, cs), "h2d images");
       ck(cudaMemcpyAsync(I.labels, labels, sizeof(int) * k, cudaMemcpyHostToDevice, cs), "h2d labels");
     } else {
       const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
@@ -678,9 +696,19 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   } else {
     kernel_launches_ = enqueue_iteration(false);
   }
+  if (next_images && host_inputs) {
+    // pipelined input: the next batch's H2D overlaps the rest of this step
+    const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
+    ck(cudaStreamWaitEvent(I.input_stream, I.layout_done, 0), "wait layout");
+    ck(cudaMemcpyAsync(I.image_nchw, next_images, img3, cudaMemcpyHostToDevice, I.input_stream),
+       "h2d next images");
+    ck(cudaEventRecord(I.input_ready, I.input_stream), "record");
+    I.prefetched = true;
+  }
   ck(cudaEventRecord(I.iter_end, cs), "record");
   ck(cudaMemcpyAsync(I.loss_host, I.loss, sizeof(float), cudaMemcpyDeviceToHost, cs), "loss d2h");
   ck(cudaStreamSynchronize(cs), "step");
+  if (I.prefetched) ck(cudaStreamSynchronize(I.input_stream), "input");
   if (update) I.first_step = false;
 
   float ms = 0.f;

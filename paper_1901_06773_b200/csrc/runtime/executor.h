@@ -72,9 +72,12 @@ class Executor {
   void get_grads(float* host, long long n);
   void get_stats(float* host, long long n);
   // images: NCHW fp32 [k][3][H][W]; labels int32 [k].  host_inputs = 1 copies
-  // from (pinned or pageable) host memory inside the step.
+  // from (pinned or pageable) host memory inside the step.  Pipelined input:
+  // next_images (host) is copied H2D on a side stream as soon as this step's
+  // layout kernel has consumed the staging buffer, overlapping the rest of
+  // the step; the next call passes images = nullptr to use it.
   StepStats step(const void* images, const int* labels, int host_inputs, float lr, int update,
-                 int profile);
+                 int profile, const void* next_images = nullptr);
   void set_comm(const void* nccl_unique_id, int rank, int world);
   bool use_graph = false;
   std::string trace_csv() const { return trace_; }

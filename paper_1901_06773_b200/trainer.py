@@ -190,6 +190,27 @@ class Executor:
         return {"loss": st.loss, "iter_ms": st.iter_ms, "exposed_swap_ms": st.exposed_swap_ms,
                 "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes}
 
+    def step_pipelined(self, images, labels, lr=0.1, update=True, next_images=None):
+        """host-input step with the next batch's H2D overlapped: images=None
+        uses the batch prefetched by the previous call; next_images (pinned
+        host tensor / array) is prefetched during this step."""
+        keep = []  # converted arrays must outlive the (synchronous) call
+
+        def ptr(a, dtype=np.float32):
+            if a is None:
+                return None
+            if hasattr(a, "data_ptr"):
+                return a.data_ptr()
+            keep.append(np.ascontiguousarray(a, dtype=dtype))
+            return keep[-1].ctypes.data
+        lp = ptr(labels, np.int32)
+        st = StepStats()
+        _check(self.lib.accudnn_exec_step_pipelined(self.h, ptr(images), lp, float(lr),
+                                                    1 if update else 0, ptr(next_images),
+                                                    ctypes.byref(st)), "step")
+        return {"loss": st.loss, "iter_ms": st.iter_ms, "exposed_swap_ms": st.exposed_swap_ms,
+                "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes}
+
     def set_comm(self, uid_bytes, rank, world):
         buf = ctypes.create_string_buffer(bytes(uid_bytes), 128)
         _check(self.lib.accudnn_exec_set_comm(self.h, buf, int(rank), int(world)), "set_comm")

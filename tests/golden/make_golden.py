@@ -10,6 +10,8 @@ tests then pin the B200 planner against them without the reference tree.
                          FNV-1a, sweep CSV
   resnet_plans.json      exported ResNet network.json + B200 profiles ->
                          per-k evaluations and small-budget full plans
+  resnet1001_plan.json   (--with-r1001, ~2 min) config 5: reference evaluations
+                         at k* and k*+1 of ResNet-1001 under 8 GiB
 """
 import ctypes
 import hashlib
@@ -103,8 +105,31 @@ def resnet_records(R):
     return out
 
 
+def resnet1001_record(R):
+    """BASELINE config 5 (ResNet-1001 @32, 8 GiB): the reference's
+    evaluate_minibatch at k* = 41 and k* + 1 (~48 s each on one core; the
+    reference's full k_max = 32,136 scan does not finish)."""
+    from paper_1901_06773_b200 import trainer
+    net, desc = trainer.export_network("resnet1001", 32, 12, k_base=8)
+    link = json.load(open(os.path.join(ROOT, "profiles", "b200", "host_link.json")))
+    hw = trainer.hardware_json(8 << 30, trainer.default_m_others(desc, 32), link["d2h"] * 1e9)
+    pdir = os.path.join(ROOT, "profiles", "b200")
+    csvs = [open(os.path.join(pdir, f"resnet1001_{k}_profile.csv")).read()
+            for k in ("compute", "transfer")]
+    model = planner.fit(net, csvs, hw, eta=0.95, **R)
+    rec = {"arch": "resnet1001", "image": 32, "classes": 12, "budget": 8 << 30,
+           "network_sha256": hashlib.sha256(net.encode()).hexdigest(), "model_json": model,
+           "hardware_json": hw, "k_max": planner.kmax(net, hw, **R), "evals": {}}
+    for k in (41, 42):
+        rec["evals"][str(k)] = planner.evaluate_k(net, hw, model, k, **R)
+    return rec
+
+
 def main():
     R = ref_lib()
+    if "--with-r1001" in sys.argv:
+        with open(os.path.join(HERE, "resnet1001_plan.json"), "w") as f:
+            json.dump(resnet1001_record(R), f, indent=1)
     fixtures = [fixture_record(s, R) for s in SEEDS]
     with open(os.path.join(HERE, "planner_fixtures.json"), "w") as f:
         json.dump(fixtures, f, indent=1)

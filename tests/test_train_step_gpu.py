@@ -177,3 +177,25 @@ def test_cuda_graph_with_swap_plan_matches_eager(cuda_dev):
         lb = b.step(x, y, lr=0.05)["loss"]
         assert la == lb
     assert np.array_equal(b.get_params(), a.get_params())
+
+
+def test_pipelined_host_input_matches_plain_steps(cuda_dev):
+    """next-batch H2D overlapped on a side stream (images=None uses the
+    prefetched batch) computes exactly what plain host-input steps compute,
+    eager and captured."""
+    arch, image, classes, k = "resnet20", 32, 12, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=8)
+    batches = [data(k, image, classes, seed=40 + i) for i in range(4)]
+    a = trainer.Executor(arch, image, classes, k=k)
+    b = trainer.Executor(arch, image, classes, k=k)
+    a.set_params(params)
+    b.set_params(params)
+    b.set_graph(True)
+    la = [a.step(x, y, lr=0.05)["loss"] for x, y in batches]
+    lb = [b.step_pipelined(batches[0][0], batches[0][1], lr=0.05, next_images=batches[1][0])["loss"]]
+    for i in range(1, 4):
+        nxt = batches[i + 1][0] if i + 1 < 4 else None
+        lb.append(b.step_pipelined(None, batches[i][1], lr=0.05, next_images=nxt)["loss"])
+    assert la == lb
+    assert np.array_equal(a.get_params(), b.get_params())
