@@ -276,7 +276,7 @@ def run_ours(args):
     if os.path.exists(lp):
         link = json.load(open(lp))
     pcie = float(link.get("d2h", 50.0)) * 1e9
-    m_others = trainer.default_m_others(desc, args.image)
+    m_others = trainer.default_m_others(desc, args.image, int(args.cap_gib * GIB))
     hardware_json = trainer.hardware_json(int(args.cap_gib * GIB), m_others, pcie)
     model_json, plan_json, plan_s, prof_src = plan_for(args, network_json, hardware_json)
     plan = json.loads(plan_json)

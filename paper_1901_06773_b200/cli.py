@@ -218,7 +218,8 @@ def cmd_export(a):
     _write(a.out, net)
     if a.hardware_out:
         hw = trainer.hardware_json(int(a.cap_gib * (1 << 30)),
-                                   trainer.default_m_others(desc, a.image), a.pcie_gbs * 1e9)
+                                   trainer.default_m_others(desc, a.image, int(a.cap_gib * (1 << 30))),
+                                   a.pcie_gbs * 1e9)
         _write(a.hardware_out, hw)
     print(f"exported {a.arch}@{a.image}: {len(desc['ops'])} layers -> {a.out}")
     return 0

@@ -67,13 +67,21 @@ def hardware_json(budget_bytes, m_others_bytes, pcie_bytes_per_s, delta_sync_s=0
                        "pcie_nominal_bytes_per_s": float(pcie_bytes_per_s)}, indent=2) + "\n"
 
 
-def default_m_others(describe, image):
+def default_m_others(describe, image, budget_bytes=None):
     """Fixed device bytes outside params+grads: the momentum buffer, BN
     statistics and a staging allowance for the input batch (the paper's
-    "pre-cached inputs and fixed overheads", PAPER.md:98)."""
+    "pre-cached inputs and fixed overheads").  The executor keeps
+    the batch twice (NCHW staging + NHWC4 for the stem, 7 floats per pixel);
+    with a budget the allowance covers the largest batch the budget could
+    hold at all (budget / featuremap bytes per image), so a tuned k* always
+    fits the executor's fixed allocations."""
     momentum = 4 * describe["n_params"]
     stats = 4 * describe["n_stats"]
     staging = (96 << 20) if image >= 128 else (32 << 20)
+    if budget_bytes:
+        fm_per_image = sum(4 * o["out"][0] * o["out"][1] * o["out"][2] for o in describe["ops"])
+        k_ub = int(budget_bytes) // max(1, fm_per_image)
+        staging = max(staging, 7 * 4 * image * image * k_ub + (8 << 20))
     return momentum + stats + staging
 
 

@@ -1,2 +1,1 @@
-timeout 600 python -m pytest tests/test_train_step_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+timeout 900 python bench.py --arch resnet50 --cap-gib 12 --steps 30 > gpurun_out/bench_r50.log 2>&1

@@ -28,7 +28,8 @@ if os.path.exists(tune):
     _native.conv_tune_import(open(tune).read())
 net, desc = trainer.export_network(arch, image, classes, k_base=8)
 link = json.load(open(os.path.join(ROOT, "profiles", "b200", "host_link.json")))
-hw = trainer.hardware_json(int(cap * (1 << 30)), trainer.default_m_others(desc, image), link["d2h"] * 1e9)
+hw = trainer.hardware_json(int(cap * (1 << 30)), trainer.default_m_others(desc, image, int(cap * (1 << 30))),
+                           link["d2h"] * 1e9)
 prof = os.path.join(ROOT, "profiles", "b200")
 model = planner.fit(net, [open(os.path.join(prof, f"{arch}_compute_profile.csv")).read(),
                           open(os.path.join(prof, f"{arch}_transfer_profile.csv")).read()], hw, eta=0.95)
