@@ -753,11 +753,16 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __r
 // of every output window and channel as one byte; (2) every input element
 // gathers dy over the <= ceil(k/stride)^2 windows covering it whose argmax
 // is this element, in window order (deterministic).
+// K, ST, PD > 0: compile-time window (the ResNet stem's 3x3 / 2 / 1: the
+// window loops unroll and every load of a thread is in flight at once);
+// 0: runtime values
+template <int K, int ST, int PD>
 __global__ void maxpool_argmax_kernel(const float* __restrict__ x, int n, int h, int w, int c4,
-                                      int kr, int ks, int stride, int pad, int p, int q,
+                                      int kr_, int ks_, int stride_, int pad_, int p, int q,
                                       uint8_t* __restrict__ arg, int total) {
   pdl_wait();
   pdl_trigger();
+  const int kr = K ? K : kr_, ks = K ? K : ks_, stride = ST ? ST : stride_, pad = K ? PD : pad_;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, channel float4)
   if (idx >= total) return;
   const int cg = idx % c4;
@@ -768,12 +773,15 @@ __global__ void maxpool_argmax_kernel(const float* __restrict__ x, int n, int h,
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   int bt[4] = {0, 0, 0, 0};
-  for (int r = 0; r < kr; ++r) {
+#pragma unroll
+  for (int r = 0; r < (K ? K : 16); ++r) {
+    if (!K && r >= kr) break;
     const int ih = pp * stride - pad + r;
-    if (ih < 0 || ih >= h) continue;
-    for (int s = 0; s < ks; ++s) {
+#pragma unroll
+    for (int s = 0; s < (K ? K : 16); ++s) {
+      if (!K && s >= ks) break;
       const int iw = qq * stride - pad + s;
-      if (iw < 0 || iw >= w) continue;
+      if (ih < 0 || ih >= h || iw < 0 || iw >= w) continue;
       const float4 v = __ldg(x4 + ((static_cast<long long>(nn) * h + ih) * w + iw) * c4 + cg);
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -789,11 +797,13 @@ __global__ void maxpool_argmax_kernel(const float* __restrict__ x, int n, int h,
   reinterpret_cast<uint32_t*>(arg)[static_cast<long long>(pix) * c4 + cg] = packed;
 }
 
+template <int K, int ST, int PD>
 __global__ void maxpool_gather_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
-                                      int n, int h, int w, int c4, int kr, int ks, int stride,
-                                      int pad, int p, int q, float* __restrict__ dx, int total) {
+                                      int n, int h, int w, int c4, int kr_, int ks_, int stride_,
+                                      int pad_, int p, int q, float* __restrict__ dx, int total) {
   pdl_wait();
   pdl_trigger();
+  const int kr = K ? K : kr_, ks = K ? K : ks_, stride = ST ? ST : stride_, pad = K ? PD : pad_;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, channel float4)
   if (idx >= total) return;
   const int cg = idx % c4;
@@ -808,22 +818,24 @@ __global__ void maxpool_gather_kernel(const uint8_t* __restrict__ arg, const flo
   const int q_hi = min(q - 1, (ww + pad) / stride);
   const uint32_t* a32 = reinterpret_cast<const uint32_t*>(arg);
   const float4* dy4 = reinterpret_cast<const float4*>(dy);
-  for (int pp = p_lo; pp <= p_hi; ++pp) {
-    for (int qq = q_lo; qq <= q_hi; ++qq) {
+  // windows covering this element: at most ceil(K/ST)^2 (2x2 for the stem)
+  constexpr int kW = K ? (K + ST - 1) / ST : 8;
+  const int np = p_hi - p_lo + 1, nq = q_hi - q_lo + 1;
+#pragma unroll
+  for (int i = 0; i < kW; ++i) {
+    if (i >= np) break;
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      if (j >= nq) break;
+      const int pp = p_lo + i, qq = q_lo + j;
       const int tap = (hh - (pp * stride - pad)) * ks + (ww - (qq * stride - pad));
       const long long o = (static_cast<long long>(nn) * p + pp) * q + qq;
       const uint32_t packed = __ldg(a32 + o * c4 + cg);
-      const bool hit[4] = {(packed & 0xFF) == static_cast<uint32_t>(tap),
-                           ((packed >> 8) & 0xFF) == static_cast<uint32_t>(tap),
-                           ((packed >> 16) & 0xFF) == static_cast<uint32_t>(tap),
-                           (packed >> 24) == static_cast<uint32_t>(tap)};
-      if (hit[0] || hit[1] || hit[2] || hit[3]) {
-        const float4 g = __ldg(dy4 + o * c4 + cg);
-        if (hit[0]) acc[0] += g.x;
-        if (hit[1]) acc[1] += g.y;
-        if (hit[2]) acc[2] += g.z;
-        if (hit[3]) acc[3] += g.w;
-      }
+      const float4 g = __ldg(dy4 + o * c4 + cg);  // loaded unconditionally: all in flight
+      if ((packed & 0xFF) == static_cast<uint32_t>(tap)) acc[0] += g.x;
+      if (((packed >> 8) & 0xFF) == static_cast<uint32_t>(tap)) acc[1] += g.y;
+      if (((packed >> 16) & 0xFF) == static_cast<uint32_t>(tap)) acc[2] += g.z;
+      if ((packed >> 24) == static_cast<uint32_t>(tap)) acc[3] += g.w;
     }
   }
   reinterpret_cast<float4*>(dx)[static_cast<long long>(pix) * c4 + cg] =
@@ -1213,16 +1225,25 @@ extern "C" int accudnn_maxpool_bwd(const float* x, const float* dy, int n, int h
   // convolutions on this stream); without one, the single-pass kernel
   const long long in4 = static_cast<long long>(n) * h * w * c4;
   const long long out4 = static_cast<long long>(n) * p * q * c4;
-  uint8_t* arg = (kr * ks <= 256 && in4 < (1LL << 31) && out4 < (1LL << 31))
+  uint8_t* arg = (kr <= 16 && ks <= 16 && (kr + stride - 1) / stride <= 8 &&
+                  (ks + stride - 1) / stride <= 8 && in4 < (1LL << 31) && out4 < (1LL << 31))
                      ? reinterpret_cast<uint8_t*>(
                            conv_splitk_workspace(static_cast<size_t>(n) * p * q * c))
                      : nullptr;
   if (arg) {
-    launch_pdl(maxpool_argmax_kernel, static_cast<unsigned>((out4 + 255) / 256), 256, 0,
-               S(stream), x, n, h, w, c4, kr, ks, stride, pad, p, q, arg, static_cast<int>(out4));
-    launch_pdl(maxpool_gather_kernel, static_cast<unsigned>((in4 + 255) / 256), 256, 0,
-               S(stream), arg, dy, n, h, w, c4, kr, ks, stride, pad, p, q, dx,
-               static_cast<int>(in4));
+    const unsigned ga = static_cast<unsigned>((out4 + 255) / 256);
+    const unsigned gg = static_cast<unsigned>((in4 + 255) / 256);
+    if (kr == 3 && ks == 3 && stride == 2 && pad == 1) {
+      launch_pdl(maxpool_argmax_kernel<3, 2, 1>, ga, 256, 0, S(stream), x, n, h, w, c4, kr, ks,
+                 stride, pad, p, q, arg, static_cast<int>(out4));
+      launch_pdl(maxpool_gather_kernel<3, 2, 1>, gg, 256, 0, S(stream), arg, dy, n, h, w, c4, kr,
+                 ks, stride, pad, p, q, dx, static_cast<int>(in4));
+    } else {
+      launch_pdl(maxpool_argmax_kernel<0, 0, 0>, ga, 256, 0, S(stream), x, n, h, w, c4, kr, ks,
+                 stride, pad, p, q, arg, static_cast<int>(out4));
+      launch_pdl(maxpool_gather_kernel<0, 0, 0>, gg, 256, 0, S(stream), arg, dy, n, h, w, c4, kr,
+                 ks, stride, pad, p, q, dx, static_cast<int>(in4));
+    }
     return static_cast<int>(cudaGetLastError());
   }
   const long long total = static_cast<long long>(n) * h * w * c4;
