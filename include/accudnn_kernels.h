@@ -65,7 +65,8 @@ int accudnn_conv_autotune(int enable);
 int accudnn_conv_tune_export(char** text);
 int accudnn_conv_tune_import(const char* text);
 /* test hook: force tile width (64/128/256), split-K factor and cluster size
- * (1, or 2 = B tile multicast across an M-tile pair) for every TMA conv
+ * (1, 2 = B tile multicast across an M-tile pair, 3 = B-stationary: the
+ * N-tile's whole B kept in shared memory) for every TMA conv
  * launch; 0 fields = automatic */
 int accudnn_conv_force_cfg(int bn, int splits, int cm);
 /* splits <= 0 picks a split-K factor automatically (TMA path: deterministic

@@ -235,7 +235,11 @@ __device__ __forceinline__ long long out_row(const Prob& a, int m) {
 // CM = 2: a cluster of two CTAs on adjacent M-tiles of the same N-tile; each
 // loads its own A and half of B, multicasting the B half to both (B traffic
 // from L2 halves); both MMA warps release a stage on both CTAs
-template <int MODE, int BN, int STAGES, int CM>
+// BS = 1 (B-stationary, split-K 1, CM 1): a CTA keeps one N-tile for all its
+// units, loads that tile's whole B (every k-block, <= ~128 KB) into shared
+// memory once, and streams only A through the ring -- half the operand
+// traffic of a 128 x BN tile for short-K GEMMs (1x1 convolutions)
+template <int MODE, int BN, int STAGES, int CM, int BS>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
@@ -244,17 +248,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool kBmn = (MODE != FWD);
   constexpr uint32_t kABytes = kBM * kBK * 4;
   constexpr uint32_t kBBytes = BN * kBK * 4;
-  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  constexpr uint32_t kStageBytes = BS ? kABytes : kABytes + kBBytes;  // ring stage
   constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  // [ring: STAGES x stage] [BS: B region, kb_total x kBBytes] [barriers] [epilogue staging]
+  const uint32_t ring_bytes =
+      STAGES * kStageBytes + (BS ? static_cast<uint32_t>(a.kb_total) * kBBytes : 0u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ring_bytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;      // BS: the stationary B tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -267,7 +275,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto decode = [&](int u, int& split, int& tile, int& tm, int& tn) {
     split = u % a.splits;
     const int pair = u / a.splits;
-    if (CM == 1) {
+    if (BS) {  // the grid is a multiple of tiles_n: u % tiles_n is fixed per CTA
+      tn = u % a.tiles_n;
+      tm = u / a.tiles_n;
+      tile = tn * a.tiles_m + tm;
+    } else if (CM == 1) {
       tile = pair;
       tm = pair % a.tiles_m;
       tn = pair / a.tiles_m;
@@ -288,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], kEpiThreads);
     }
+    ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -312,6 +325,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ============================ TMA producers ============================
       const uint32_t pid = warp == 0 ? 0u : static_cast<uint32_t>(warp - 5);
       uint32_t kc = 0;  // k-blocks of this CTA (ring position)
+      if (BS && pid == 0 && cid < a.units) {
+        // the whole B tile of this CTA's N-tile, every k-block, once
+        const int n0 = (cid % a.tiles_n) * BN;
+        const uint32_t sBs = smem_base + STAGES * kStageBytes;
+        mbar_expect_tx(bfull, static_cast<uint32_t>(a.kb_total) * kBBytes);
+        for (int kb = 0; kb < a.kb_total; ++kb) {
+          const uint32_t sB = sBs + kb * kBBytes;
+          const int kk = kb * kBK;
+          if constexpr (MODE == FWD) {
+            tma_2d(&tmB, sB, bfull, kk, n0);
+          } else if constexpr (MODE == DGRAD) {
+            const int t = kk / a.K, co0 = kk - t * a.K;
+            const int tr = t / a.Sc, ts = t - tr * a.Sc;
+            const int tap = (a.r0 - a.stride * tr) * a.S + (a.s0 - a.stride * ts);
+            if (a.b_packed) {
+              tma_4d(&tmB, sB, bfull, 0, co0, n0 / 32, tap);
+            } else {
+#pragma unroll
+              for (int b = 0; b < BN / 32; ++b)
+                tma_3d(&tmB, sB + b * 4096, bfull, n0 + 32 * b, tap, co0);
+            }
+          }
+        }
+      }
       for (int u = cid; u < a.units; u += ncl) {
         int split, tile, tm, tn;
         decode(u, split, tile, tm, tn);
@@ -345,7 +382,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t* bar = &full[stage];
           mbar_expect_tx(bar, kStageBytes);
           const int kk = kb * kBK;
-          if constexpr (MODE == FWD) {
+          if constexpr (BS && MODE == FWD) {  // A only
+            if (a.a_tiled) {
+              tma_2d(&tmA, sA, bar, kk, m0);
+            } else {
+              const int tap = kk / a.C, c0 = kk - tap * a.C;
+              const int r = tap / a.S, s = tap - r * a.S;
+              tma_im2col(&tmA, sA, bar, c0, pj * a.stride - a.pad, pi * a.stride - a.pad, pn,
+                         static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            }
+          } else if constexpr (BS && MODE == DGRAD) {
+            const int t = kk / a.K, co0 = kk - t * a.K;
+            const int tr = t / a.Sc, ts = t - tr * a.Sc;
+            if (a.a_tiled) {
+              tma_2d(&tmA, sA, bar, co0, m0);
+            } else {
+              tma_im2col(&tmA, sA, bar, co0, pj + a.lo_w, pi + a.lo_h, pn,
+                         static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
+            }
+          } else if constexpr (MODE == FWD) {
             if (a.a_tiled) {
               tma_2d(&tmA, sA, bar, kk, m0);
             } else {
@@ -415,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = ptx::idesc_tf32(kBM, BN, kAmn, kBmn);
       uint32_t kc = 0;
       int j = 0;  // units processed by this CTA
+      if (BS && cid < a.units) ptx::mbar_wait(bfull, 0);
       for (int u = cid; u < a.units; u += ncl, ++j) {
         const int split = u % a.splits;
         const int kb0 = split * a.kb_per_split;
@@ -429,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (a.trace && kc < 256) a.trace[blockIdx.x * 1024 + 256 + kc] = clock64();
           ptx::tc_fence_after();
           const uint32_t sA = smem_base + stage * kStageBytes;
-          const uint32_t sB = sA + kABytes;
+          const uint32_t sB = BS ? smem_base + STAGES * kStageBytes + kb * kBBytes : sA + kABytes;
 #pragma unroll
           for (int ks = 0; ks < kBK / 8; ++ks) {
             const uint64_t ad = kAmn ? ptx::smem_desc(sA + ks * 1024, 4096, 512, 1)
@@ -457,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 128-byte row segments from the same smem transpose instead.
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int ew = warp - 2;    // staging buffers of this warp
-    float* stage_buf = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 1024) + ew * 2048;
+    float* stage_buf = reinterpret_cast<float*>(smem + ring_bytes + 1024) + ew * 2048;
     const uint32_t sbuf0 = ptx::smem_u32(stage_buf);
     const int rr_lo = lane >> 3;  // read-back row within a group of 4 (scatter path)
     const int gg = lane & 7;      // read-back 16-byte granule
@@ -802,20 +858,24 @@ int choose_splits(long long tiles, int kb_total, int bn, long long out_elems, in
   return best;
 }
 
-template <int MODE, int BN, int STAGES, int CM>
+template <int MODE, int BN, int STAGES, int CM, int BS>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
              cudaStream_t st) {
-  constexpr size_t smem = STAGES * (kBM + BN) * kBK * 4 + 1024 + 1024 + 4 * 8192;
+  const size_t ring = BS ? STAGES * kBM * kBK * 4 + static_cast<size_t>(a.kb_total) * BN * kBK * 4
+                         : STAGES * (kBM + BN) * kBK * 4;
+  const size_t smem = ring + 1024 + 1024 + 4 * 8192;
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM>,
+    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem));
+                                               227 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
     configured = true;
   }
-  const int grid =
-      CM * static_cast<int>(std::min<long long>(a.units, sm_count() / CM));
+  if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidValue);
+  int grid = CM * static_cast<int>(std::min<long long>(a.units, sm_count() / CM));
+  if (BS) grid = std::min(sm_count(), a.units) / a.tiles_n * a.tiles_n;  // fixed N-tile per CTA
+  if (grid < 1) return static_cast<int>(cudaErrorInvalidValue);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -830,7 +890,8 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CM > 1 ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM>, ta, tb, tc, a);
+  cudaError_t e =
+      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
   if (a.stats) {
@@ -887,7 +948,9 @@ struct Call {
 struct Cfg {
   int bn = 0, splits = 0;
   int cm = 1;  // CTAs per cluster sharing the B tile by multicast (1 or 2; FWD / DGRAD)
+  int bs = 0;  // B-stationary (FWD / DGRAD, splits 1, cm 1, B tile <= kMaxBStat bytes)
 };
+constexpr size_t kMaxBStat = 128 * 1024;
 struct KeyHash {
   size_t operator()(const std::array<int, 14>& k) const {
     size_t h = 1469598103934665603ull;
@@ -995,12 +1058,17 @@ bool encode(const Call& c, int bn, int cm, CUtensorMap* ta, CUtensorMap* tb, Pro
                     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int MODE, int CM>
+template <int MODE, int CM, int BS>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
                 int bn, cudaStream_t st) {
-  if (bn == 256) return launch_t<MODE, 256, 4, CM>(ta, tb, tc, a, st);
-  if (bn == 128) return launch_t<MODE, 128, 6, CM>(ta, tb, tc, a, st);
-  return launch_t<MODE, 64, 8, CM>(ta, tb, tc, a, st);
+  if (BS) {  // A-only ring of 4 x 16 KB; B lives in its own region
+    if (bn == 256) return launch_t<MODE, 256, 4, CM, BS>(ta, tb, tc, a, st);
+    if (bn == 128) return launch_t<MODE, 128, 4, CM, BS>(ta, tb, tc, a, st);
+    return launch_t<MODE, 64, 4, CM, BS>(ta, tb, tc, a, st);
+  }
+  if (bn == 256) return launch_t<MODE, 256, 4, CM, BS>(ta, tb, tc, a, st);
+  if (bn == 128) return launch_t<MODE, 128, 6, CM, BS>(ta, tb, tc, a, st);
+  return launch_t<MODE, 64, 8, CM, BS>(ta, tb, tc, a, st);
 }
 
 // -1: could not encode the tensor maps (not launched)
@@ -1008,6 +1076,9 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   CUtensorMap ta, tb;
   Prob a = c.a;
   if (c.mode == WGRAD) cfg.cm = 1;  // multicast of B across M-tiles: FWD / DGRAD only
+  if (cfg.bs && (c.mode == WGRAD || cfg.splits != 1 || cfg.cm != 1 ||
+                 static_cast<size_t>(c.a.kb_total) * cfg.bn * kBK * 4 > kMaxBStat))
+    cfg.bs = 0;
   if (!encode(c, cfg.bn, cfg.cm, &ta, &tb, a)) return -1;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (a.Ng + cfg.bn - 1) / cfg.bn;
@@ -1035,13 +1106,16 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
     const cuuint32_t box[2] = {32, 32};
     a.tma_out = tiled_map(&tc, a.out, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
   }
+  if (cfg.bs && a.tiles_n > sm_count()) cfg.bs = 0;
   if (c.mode == FWD)
-    return cfg.cm > 1 ? dispatch_bn<FWD, 2>(ta, tb, tc, a, cfg.bn, st)
-                      : dispatch_bn<FWD, 1>(ta, tb, tc, a, cfg.bn, st);
+    return cfg.bs ? dispatch_bn<FWD, 1, 1>(ta, tb, tc, a, cfg.bn, st)
+                  : cfg.cm > 1 ? dispatch_bn<FWD, 2, 0>(ta, tb, tc, a, cfg.bn, st)
+                               : dispatch_bn<FWD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
   if (c.mode == DGRAD)
-    return cfg.cm > 1 ? dispatch_bn<DGRAD, 2>(ta, tb, tc, a, cfg.bn, st)
-                      : dispatch_bn<DGRAD, 1>(ta, tb, tc, a, cfg.bn, st);
-  return dispatch_bn<WGRAD, 1>(ta, tb, tc, a, cfg.bn, st);
+    return cfg.bs ? dispatch_bn<DGRAD, 1, 1>(ta, tb, tc, a, cfg.bn, st)
+                  : cfg.cm > 1 ? dispatch_bn<DGRAD, 2, 0>(ta, tb, tc, a, cfg.bn, st)
+                               : dispatch_bn<DGRAD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
+  return dispatch_bn<WGRAD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
 }
 
 bool splits_ok(const Call& c, int s) {
@@ -1077,13 +1151,20 @@ Cfg tune(const Call& c, cudaStream_t st) {
   cudaEventCreate(&e1);
   Cfg best = model_cfg(c);
   float best_ms = 1e30f;
-  for (int cm : {1, 2}) {
-   if (cm > 1 && c.mode == WGRAD) continue;
+  // 0: plain, 1: 2-CTA multicast.  (2, B-stationary, is available through
+  // accudnn_conv_force_cfg but not tuned: measured no faster -- the k-block
+  // rate is bound by bytes in flight per SM x memory latency, not by B traffic)
+  for (int variant : {0, 1}) {
+   const int cm = variant == 1 ? 2 : 1;
+   const int bs = variant == 2 ? 1 : 0;
+   if (variant > 0 && c.mode == WGRAD) continue;
    for (int bn : {64, 128, 256}) {
     if (!bn_ok(c, bn)) continue;
+    if (bs && static_cast<size_t>(c.a.kb_total) * bn * kBK * 4 > kMaxBStat) continue;
     for (int s : kSplits) {
       if (!splits_ok(c, s)) continue;
-      const Cfg cand{bn, s, cm};
+      if (bs && s != 1) continue;
+      const Cfg cand{bn, s, cm, bs};
       if (launch_cfg(c, cand, st) != 0) {
         cudaGetLastError();
         continue;
@@ -1117,7 +1198,11 @@ int run_call(const Call& c, cudaStream_t st) {
     Cfg f = model_cfg(c);
     if (g_force.bn > 0 && bn_ok(c, g_force.bn)) f.bn = g_force.bn;
     if (g_force.splits > 0 && splits_ok(c, g_force.splits)) f.splits = g_force.splits;
-    if (g_force.cm > 0) f.cm = g_force.cm;
+    if (g_force.cm > 0) f.cm = g_force.cm == 3 ? 1 : g_force.cm;
+    if (g_force.cm == 3) {  // test hook: B-stationary
+      f.bs = 1;
+      f.splits = 1;
+    }
     return launch_cfg(c, f, st);
   }
   std::array<int, 14> key;
@@ -1335,7 +1420,7 @@ extern "C" int accudnn_conv_tune_export(char** out) {
   for (const auto& kv : accudnn::g_tuned) {
     for (int v : kv.first) t += std::to_string(v) + " ";
     t += std::to_string(kv.second.bn) + " " + std::to_string(kv.second.splits) + " " +
-         std::to_string(kv.second.cm) + "\n";
+         std::to_string(kv.second.cm) + " " + std::to_string(kv.second.bs) + "\n";
   }
   char* buf = static_cast<char*>(std::malloc(t.size() + 1));
   if (!buf) return static_cast<int>(cudaErrorMemoryAllocation);
@@ -1357,6 +1442,7 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
     if (!ok) continue;
     if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2)) cfg.cm = 1;
+    if (!(ls >> cfg.bs) || (cfg.bs != 0 && cfg.bs != 1)) cfg.bs = 0;
     if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;
     if (cfg.splits < 1) continue;
     accudnn::g_tuned[key] = cfg;

@@ -63,7 +63,7 @@ def check(got, ref):
     assert (got - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-6
 
 
-@pytest.fixture(params=["tma", "tma_cluster2", "tma_bn64_split3", "cpasync"])
+@pytest.fixture(params=["tma", "tma_cluster2", "tma_bn64_split3", "tma_bstat", "cpasync"])
 def impl(request):
     """TMA kernel with the analytic config, with the B tile multicast across an
     M-tile pair (cluster of 2), with narrow tiles + forced split-K, and the
@@ -74,6 +74,8 @@ def impl(request):
         lib.accudnn_conv_force_cfg(0, 0, 2)
     elif request.param == "tma_bn64_split3":
         lib.accudnn_conv_force_cfg(64, 3, 1)
+    elif request.param == "tma_bstat":  # B-stationary where the B tile fits, else analytic
+        lib.accudnn_conv_force_cfg(64, 0, 3)
     yield request.param
     lib.accudnn_conv_force_cfg(0, 0, 0)
     lib.accudnn_set_conv_impl(1)
@@ -209,6 +211,7 @@ def test_dgrad_strided_accumulate(cuda_dev, shape):
 
 
 @pytest.mark.parametrize("shape,forced", [((8, 256, 14, 14, 1024, 1, 1, 0), (0, 0, 0)),
+                                          ((8, 256, 14, 14, 1024, 1, 1, 0), (128, 0, 3)),
                                           ((27, 1024, 14, 14, 256, 1, 1, 0), (256, 4, 1)),
                                           ((4, 64, 28, 28, 64, 3, 1, 1), (0, 0, 2)),
                                           ((3, 96, 10, 10, 160, 3, 1, 1), (0, 0, 0))])
