@@ -38,6 +38,7 @@
 namespace accudnn {
 // split-K workspace + slice-order reduction (conv_sm100.cu)
 float* conv_splitk_workspace(size_t bytes);
+void conv_select_workspace(cudaStream_t st);
 int conv_splitk_reduce(float* ws, int splits, int M, int Ng, float* out, int beta,
                        cudaStream_t st);
 namespace {
@@ -524,6 +525,7 @@ using namespace accudnn;
 extern "C" int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, const float* w,
                                 float* y, int beta, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  conv_select_workspace(stream);
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
   int rc = 0;
   if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_fwd(d, x, w, y, beta, stream, &rc))
@@ -539,6 +541,7 @@ extern "C" int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, cons
 extern "C" int accudnn_conv_fwd_stats(const accudnn_conv_desc* d, const float* x, const float* w,
                                       float* y, float* stats, int* produced, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  conv_select_workspace(stream);
   *produced = 0;
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
   int rc = 0;
@@ -552,6 +555,7 @@ extern "C" int accudnn_conv_fwd_stats(const accudnn_conv_desc* d, const float* x
 extern "C" int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w,
                                   float* dx, int beta, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  conv_select_workspace(stream);
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
   int rc = 0;
   if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_dgrad(d, dy, w, dx, beta, stream, &rc))
@@ -564,6 +568,7 @@ extern "C" int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, c
 extern "C" int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy,
                                   float* dw, int beta, int splits, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  conv_select_workspace(stream);
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
   int rc = 0;
   if (g_conv_impl == 1 && g_conv_math == 0 && splits <= 0 &&

@@ -815,10 +815,19 @@ struct Workspace {
 };
 Workspace g_ws;
 size_t g_ws_default = 64ull << 20;
+// per-stream workspaces (a concurrent weight-gradient stream must not share
+// the compute stream's split-K partials); the entry points select the one
+// of their stream before any split-K decision
+struct StreamWs {
+  cudaStream_t st = nullptr;
+  Workspace w;
+};
+StreamWs g_stream_ws[4];
+Workspace* g_cur = &g_ws;
 long long* g_trace = nullptr;  // debug stamps, see accudnn_conv_trace
 
 // lazily owned workspace when the caller did not provide one
-size_t ws_capacity() {
+size_t default_ws_capacity() {
   if (!g_ws.ws && !g_ws.bytes && g_ws_default) {
     if (cudaMalloc(&g_ws.ws, g_ws_default) == cudaSuccess) {
       g_ws.bytes = g_ws_default;
@@ -830,6 +839,7 @@ size_t ws_capacity() {
   }
   return g_ws.ws ? g_ws.bytes : 0;
 }
+size_t ws_capacity() { return g_cur == &g_ws ? default_ws_capacity() : g_cur->bytes; }
 
 // Split-K factor from a makespan model in SM cycles: a persistent CTA pays
 // a prologue, then waves of units (k-blocks of 2*BN + 128 cycles each plus a
@@ -1085,7 +1095,7 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   a.splits = cfg.splits;
   a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
   a.units = (cfg.cm > 1 ? (a.tiles_m + 1) / 2 : a.tiles_m) * a.tiles_n * a.splits;
-  a.ws = g_ws.ws;
+  a.ws = g_cur->ws;
   a.trace = g_trace;
   // output tensor map for the bulk-store epilogue: the split-K workspace
   // {Ng, M, S} (rows past M clip inside their own slice) or the row-major
@@ -1368,10 +1378,16 @@ int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, 
   return 1;
 }
 
+void conv_select_workspace(cudaStream_t st) {
+  g_cur = &g_ws;
+  for (StreamWs& e : g_stream_ws)
+    if (e.st && e.st == st && e.w.ws) g_cur = &e.w;
+}
+
 // shared with the cp.async kernel (conv_igemm.cu): the split-K workspace if
 // it holds `bytes`, else nullptr; and the slice-order reduction on it
 float* conv_splitk_workspace(size_t bytes) {
-  return ws_capacity() >= bytes ? g_ws.ws : nullptr;
+  return ws_capacity() >= bytes ? g_cur->ws : nullptr;
 }
 int conv_splitk_reduce(float* ws, int splits, int M, int Ng, float* out, int beta,
                        cudaStream_t st) {
@@ -1402,6 +1418,31 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
   g_ws.owned = false;
   if (!ptr) g_ws_default = static_cast<size_t>(bytes);
   return 0;
+}
+
+// a split-K workspace used only by convolutions launched on `stream` (e.g.
+// weight gradients on a side stream running concurrently with the compute
+// stream); ptr == NULL removes the stream's entry
+extern "C" int accudnn_conv_set_stream_workspace(void* stream, void* ptr,
+                                                 unsigned long long bytes) {
+  using namespace accudnn;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!st) return static_cast<int>(cudaErrorInvalidValue);
+  for (StreamWs& e : g_stream_ws)
+    if (e.st == st) {
+      e = StreamWs{};
+      if (!ptr) return 0;
+      break;
+    }
+  if (!ptr) return 0;
+  for (StreamWs& e : g_stream_ws)
+    if (!e.st) {
+      e.st = st;
+      e.w.ws = static_cast<float*>(ptr);
+      e.w.bytes = static_cast<size_t>(bytes);
+      return 0;
+    }
+  return static_cast<int>(cudaErrorMemoryAllocation);
 }
 
 // debug: subsequent TMA-conv launches record clock64 stamps into buf

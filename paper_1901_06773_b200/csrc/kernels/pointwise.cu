@@ -19,6 +19,7 @@
 namespace accudnn {
 int g_pdl = 0;  // measured: PDL slowed the captured step (19.6 vs 18.9 ms), off by default
 float* conv_splitk_workspace(size_t bytes);  // conv_sm100.cu
+void conv_select_workspace(cudaStream_t st);
 namespace {
 
 constexpr int kThreads = 256;
@@ -1221,6 +1222,7 @@ extern "C" int accudnn_maxpool_bwd(const float* x, const float* dy, int n, int h
                                    void* stream) {
   if (c & 3) return static_cast<int>(cudaErrorInvalidValue);
   const int c4 = c / 4;
+  conv_select_workspace(S(stream));
   // argmax bytes live in the convolution split-K workspace (idle between
   // convolutions on this stream); without one, the single-pass kernel
   const long long in4 = static_cast<long long>(n) * h * w * c4;

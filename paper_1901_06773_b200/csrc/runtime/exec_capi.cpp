@@ -90,6 +90,8 @@ int accudnn_exec_create(const char* arch, int image, int classes, const char* mo
     cfg.classes = classes;
     cfg.device = device;
     cfg.lookahead = lookahead;
+    // ACCUDNN_WGRAD_STREAM=0: weight gradients in line on the compute stream
+    if (const char* e = std::getenv("ACCUDNN_WGRAD_STREAM")) cfg.wgrad_stream = std::atoi(e);
     const accudnn::Net net = accudnn::build_net(arch, image, classes);
     const int n = net.num_ops();
     const std::string m = mode ? mode : "resident";

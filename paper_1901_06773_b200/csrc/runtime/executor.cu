@@ -58,6 +58,11 @@ struct Executor::Impl {
   // streams / events
   cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr, comm_stream = nullptr;
   cudaStream_t input_stream = nullptr;  // pipelined next-batch H2D
+  cudaStream_t side = nullptr;          // concurrent weight gradients
+  void* side_ws = nullptr;              // its split-K workspace
+  std::vector<cudaEvent_t> fork_ev;     // per step: dy ready on the compute stream
+  std::vector<cudaEvent_t> wg_done;     // per step: that step's weight gradient done
+  std::vector<int> side_last;           // per instance: last step whose wgrad reads it
   cudaEvent_t layout_done = nullptr;    // staging buffer consumed (record node in the graph)
   cudaEvent_t input_ready = nullptr;    // next batch landed in the staging buffer
   bool prefetched = false;
@@ -159,6 +164,12 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
     conv_ws &= ~static_cast<size_t>(4095);
   }
   fixed_bytes_ += conv_ws;
+  // the side stream's weight gradients get their own share of it
+  size_t side_ws = 0;
+  if (cfg.wgrad_stream && conv_ws) {
+    side_ws = (conv_ws / 2) & ~static_cast<size_t>(4095);
+    conv_ws -= side_ws;
+  }
   if (cfg.budget) {
     if (cfg.fixed_allowance && fixed_bytes_ > cfg.fixed_allowance)
       throw std::runtime_error("fixed device allocations (" + std::to_string(fixed_bytes_) +
@@ -181,6 +192,7 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaMalloc(&I.loss, 256), "loss");
   ck(cudaMallocHost(&I.loss_host, sizeof(float)), "loss host");
   if (conv_ws) ck(cudaMalloc(&I.conv_ws, conv_ws), "conv workspace");
+  if (side_ws) ck(cudaMalloc(&I.side_ws, side_ws), "side conv workspace");
   if (I.bn_stats_bytes)
     for (auto& p : I.bn_stats) ck(cudaMalloc(&p, I.bn_stats_bytes), "bn stats");
   I.stats_from_conv.assign(static_cast<size_t>(n), 0);
@@ -231,6 +243,9 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaStreamCreateWithFlags(&I.h2d, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.comm_stream, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.input_stream, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&I.side, cudaStreamNonBlocking), "stream");
+  if (I.side_ws)
+    ckl(accudnn_conv_set_stream_workspace(I.side, I.side_ws, side_ws), "side workspace");
   ck(cudaEventCreateWithFlags(&I.layout_done, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&I.input_ready, cudaEventDisableTiming), "event");
   auto mk = [](std::vector<cudaEvent_t>& v, size_t cnt, bool timing) {
@@ -242,6 +257,27 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   mk(I.step_done, static_cast<size_t>(2 * n + 2), false);
   mk(I.d2h_done, static_cast<size_t>(n), false);
   mk(I.h2d_done, static_cast<size_t>(n), false);
+  mk(I.fork_ev, static_cast<size_t>(2 * n + 2), false);
+  mk(I.wg_done, static_cast<size_t>(2 * n + 2), false);
+  // instances a side-stream weight gradient reads (its input activation as
+  // the backward step sees it, and the output gradient): a later occupant of
+  // their bytes must also wait for that weight gradient
+  I.side_last.assign(I.lm.inst.size(), 0);
+  for (int s = n + 1; s <= 2 * n; ++s)
+  for (int o : {2 * n + 1 - s, s == 2 * n ? 0 : -1}) {  // the ops of step s (see step())
+    if (o < 0 || o >= n || (o == 0 && s != 2 * n)) continue;
+    const Op& op = net_.ops[static_cast<size_t>(o)];
+    if (op.kind != OpKind::conv && op.kind != OpKind::fc) continue;
+    if (op.in0 >= 0) {
+      const size_t u = static_cast<size_t>(op.in0);
+      int id = I.lm.act_inst[u];
+      if (I.lm.pre_inst[u] >= 0 && s >= I.lm.inst[static_cast<size_t>(I.lm.pre_inst[u])].first)
+        id = I.lm.pre_inst[u];
+      if (id >= 0) I.side_last[static_cast<size_t>(id)] = std::max(I.side_last[static_cast<size_t>(id)], s);
+    }
+    const int g = I.lm.grad_inst[static_cast<size_t>(o)];
+    if (g >= 0) I.side_last[static_cast<size_t>(g)] = std::max(I.side_last[static_cast<size_t>(g)], s);
+  }
   mk(I.phase_begin, static_cast<size_t>(2 * n + 2), true);
   mk(I.phase_end, static_cast<size_t>(2 * n + 2), true);
   ck(cudaEventCreate(&I.iter_begin), "event");
@@ -253,13 +289,14 @@ Executor::~Executor() {
   Impl& I = *impl_;
   if (I.graph) cudaGraphExecDestroy(I.graph);
   if (I.comm) ncclCommDestroy(I.comm);
+  if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0);
   for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
-                  &I.bucket_ready})
+                  &I.bucket_ready, &I.fork_ev, &I.wg_done})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done, I.layout_done, I.input_ready})
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {I.compute, I.d2h, I.h2d, I.comm_stream, I.input_stream})
+  for (cudaStream_t s : {I.compute, I.d2h, I.h2d, I.comm_stream, I.input_stream, I.side})
     if (s) cudaStreamDestroy(s);
   for (float* h : I.host_store)
     if (h) cudaFreeHost(h);
@@ -269,7 +306,7 @@ Executor::~Executor() {
                   static_cast<void*>(I.stats), I.bn_ws, static_cast<void*>(I.image),
                   static_cast<void*>(I.image_nchw), static_cast<void*>(I.labels),
                   static_cast<void*>(I.loss), I.conv_ws, static_cast<void*>(I.bn_stats[0]),
-                  static_cast<void*>(I.bn_stats[1])})
+                  static_cast<void*>(I.bn_stats[1]), I.side_ws})
     if (p) cudaFree(p);
   if (I.conv_ws || cfg_.budget) accudnn_conv_set_workspace(nullptr, 64ull << 20);
 }
@@ -311,6 +348,8 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   cudaStream_t cs = I.compute;
   void* csv = static_cast<void*>(cs);
   StepStats st;
+  const bool use_side = cfg_.wgrad_stream && !profile && !I.first_step;
+  int last_wg = 0;  // latest step with a side-stream weight gradient
 
   auto act = [&](int t, int step) -> float* {
     if (t == kImage) return I.image;
@@ -436,7 +475,17 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       case OpKind::fc: {
         const accudnn_conv_desc d = conv_desc(op);
         float* dy = grad(o);
-        ckl(accudnn_conv_wgrad(&d, act(op.in0, s), dy, I.grads + op.w_off, 0, 0, csv), "wgrad");
+        if (use_side) {
+          ck(cudaEventRecord(I.fork_ev[static_cast<size_t>(s)], cs), "record");
+          ck(cudaStreamWaitEvent(I.side, I.fork_ev[static_cast<size_t>(s)], 0), "wait");
+          ckl(accudnn_conv_wgrad(&d, act(op.in0, s), dy, I.grads + op.w_off, 0, 0,
+                                 static_cast<void*>(I.side)),
+              "wgrad");
+          ck(cudaEventRecord(I.wg_done[static_cast<size_t>(s)], I.side), "record");
+          last_wg = s;
+        } else {
+          ckl(accudnn_conv_wgrad(&d, act(op.in0, s), dy, I.grads + op.w_off, 0, 0, csv), "wgrad");
+        }
         if (op.in0 != kImage)
           ckl(accudnn_conv_dgrad(&d, dy, I.params + op.w_off, grad(op.in0), beta_for(op.in0, o),
                                  csv),
@@ -512,6 +561,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   auto wait_region = [&](int inst, cudaStream_t stream, bool same_as_compute) {
     for (int p : I.preds[static_cast<size_t>(inst)]) {
       const Instance& y = I.lm.inst[static_cast<size_t>(p)];
+      if (use_side && I.side_last[static_cast<size_t>(p)] > 0)
+        ck(cudaStreamWaitEvent(stream, I.wg_done[static_cast<size_t>(I.side_last[static_cast<size_t>(p)])], 0),
+           "wait wgrad");
       if (y.kind == InstKind::act && y.swapped) {
         ck(cudaStreamWaitEvent(stream, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
         if (same_as_compute) swap_wait[static_cast<size_t>(cur_step)] = 1;
@@ -571,6 +623,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
         // region free: every earlier occupant finished (compute) and drained
         for (int q : I.preds[static_cast<size_t>(pid)]) {
           const Instance& y = I.lm.inst[static_cast<size_t>(q)];
+          if (use_side && I.side_last[static_cast<size_t>(q)] > 0)
+            ck(cudaStreamWaitEvent(I.h2d, I.wg_done[static_cast<size_t>(I.side_last[static_cast<size_t>(q)])], 0),
+               "wait wgrad");
           if (y.kind == InstKind::act && y.swapped)
             ck(cudaStreamWaitEvent(I.h2d, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
           ck(cudaStreamWaitEvent(I.h2d, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
@@ -629,6 +684,8 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
         const long long ready = prefix_after_step[static_cast<size_t>(s)];
         if (ready - reduced >= bucket || (s == 2 * n && ready > reduced)) {
           ck(cudaStreamWaitEvent(I.comm_stream, I.step_done[static_cast<size_t>(s)], 0), "wait");
+          if (last_wg > 0)
+            ck(cudaStreamWaitEvent(I.comm_stream, I.wg_done[static_cast<size_t>(last_wg)], 0), "wait");
           ckn(ncclAllReduce(I.grads + reduced, I.grads + reduced,
                             static_cast<size_t>(ready - reduced), ncclFloat, ncclSum, I.comm,
                             I.comm_stream),
@@ -642,7 +699,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       ck(cudaEventRecord(I.comm_done, I.comm_stream), "record");
       ck(cudaStreamWaitEvent(cs, I.comm_done, 0), "wait");
     }
-    // the copy streams rejoin the compute stream (graph capture needs it)
+    // the weight-gradient and copy streams rejoin the compute stream (graph
+    // capture needs it; the update reads every gradient)
+    if (last_wg > 0) ck(cudaStreamWaitEvent(cs, I.wg_done[static_cast<size_t>(last_wg)], 0), "join");
     bool any_swap = false;
     for (char c : I.swapped) any_swap = any_swap || c;
     if (any_swap) {

@@ -48,6 +48,11 @@ struct ExecConfig {
   // k*=42: 2218 vs 2243 img/s -- the epilogue cost exceeds the saved read --
   // so off by default.
   int conv_bn_stats = 0;
+  // weight gradients on a side stream, concurrent with the data-gradient
+  // chain (dgrad -> BN backward -> ...), which is the critical path; the
+  // weight gradients are only needed by the all-reduce and the update.
+  // Not used in profiled or autotuning (first) steps.
+  int wgrad_stream = 1;
 };
 
 struct StepStats {

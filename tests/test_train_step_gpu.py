@@ -199,3 +199,35 @@ def test_pipelined_host_input_matches_plain_steps(cuda_dev):
         lb.append(b.step_pipelined(None, batches[i][1], lr=0.05, next_images=nxt)["loss"])
     assert la == lb
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+@pytest.mark.parametrize("mode", ["resident", "dynamic"])
+def test_wgrad_side_stream_matches_inline(cuda_dev, mode):
+    """weight gradients on the concurrent side stream (default) compute exactly
+    what the in-line order computes, eager and captured, with the arena's
+    region reuse and (dynamic) offload/prefetch copies waiting on them."""
+    arch, image, classes, k = "resnet50", 64, 8, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    n = len(desc["ops"])
+    plan = None
+    if mode == "dynamic":
+        plan = json.dumps({"k_star": k, "pinned_objects": [f"fm{l}" for l in range(1, n + 1, 3)]})
+    params = trainer.init_params(desc, seed=9)
+    os.environ["ACCUDNN_WGRAD_STREAM"] = "0"
+    try:
+        a = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan)
+    finally:
+        del os.environ["ACCUDNN_WGRAD_STREAM"]
+    b = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan)
+    c = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan)
+    for e in (a, b, c):
+        e.set_params(params)
+    c.set_graph(True)
+    for it in range(4):
+        x, y = data(k, image, classes, seed=50 + it)
+        la = a.step(x, y, lr=0.05)["loss"]
+        lb = b.step(x, y, lr=0.05)["loss"]
+        lc = c.step(x, y, lr=0.05)["loss"]
+        assert la == lb == lc, (it, la, lb, lc)
+    assert np.array_equal(a.get_params(), b.get_params())
+    assert np.array_equal(a.get_params(), c.get_params())
