@@ -288,7 +288,7 @@ def run_ours(args):
     # profiles; shapes it lacks are tuned in the first (eager) step
     from paper_1901_06773_b200 import _native
     tune_path = os.path.join(ROOT, "profiles", "b200", "conv_tune.txt")
-    if os.path.exists(tune_path):
+    if os.path.exists(tune_path) and not os.environ.get("ACCUDNN_RETUNE"):
         _native.conv_tune_import(open(tune_path).read())
     ex = trainer.Executor(args.arch, args.image, args.classes, mode="dynamic", plan_json=plan_json,
                           network_json=network_json, hardware_json=hardware_json, device=local)

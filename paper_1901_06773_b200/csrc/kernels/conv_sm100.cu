@@ -821,9 +821,12 @@ size_t g_ws_default = 64ull << 20;
 struct StreamWs {
   cudaStream_t st = nullptr;
   Workspace w;
+  int max_ctas = 0;  // persistent grids on this stream use at most this many SMs (0: all)
 };
 StreamWs g_stream_ws[4];
 Workspace* g_cur = &g_ws;
+int g_cur_ctas = 0;
+int cta_slots() { return g_cur_ctas > 0 ? std::min(g_cur_ctas, sm_count()) : sm_count(); }
 long long* g_trace = nullptr;  // debug stamps, see accudnn_conv_trace
 
 // lazily owned workspace when the caller did not provide one
@@ -883,8 +886,8 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
     configured = true;
   }
   if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidValue);
-  int grid = CM * static_cast<int>(std::min<long long>(a.units, sm_count() / CM));
-  if (BS) grid = std::min(sm_count(), a.units) / a.tiles_n * a.tiles_n;  // fixed N-tile per CTA
+  int grid = CM * static_cast<int>(std::min<long long>(a.units, cta_slots() / CM));
+  if (BS) grid = std::min(cta_slots(), a.units) / a.tiles_n * a.tiles_n;  // fixed N-tile per CTA
   if (grid < 1) return static_cast<int>(cudaErrorInvalidValue);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1380,8 +1383,12 @@ int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, 
 
 void conv_select_workspace(cudaStream_t st) {
   g_cur = &g_ws;
+  g_cur_ctas = 0;
   for (StreamWs& e : g_stream_ws)
-    if (e.st && e.st == st && e.w.ws) g_cur = &e.w;
+    if (e.st && e.st == st) {
+      if (e.w.ws) g_cur = &e.w;
+      g_cur_ctas = e.max_ctas;
+    }
 }
 
 // shared with the cp.async kernel (conv_igemm.cu): the split-K workspace if
@@ -1422,24 +1429,25 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
 
 // a split-K workspace used only by convolutions launched on `stream` (e.g.
 // weight gradients on a side stream running concurrently with the compute
-// stream); ptr == NULL removes the stream's entry
+// stream) and a cap on their persistent grids (max_ctas SMs, 0 = all);
+// ptr == NULL and max_ctas == 0 removes the stream's entry
 extern "C" int accudnn_conv_set_stream_workspace(void* stream, void* ptr,
-                                                 unsigned long long bytes) {
+                                                 unsigned long long bytes, int max_ctas) {
   using namespace accudnn;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!st) return static_cast<int>(cudaErrorInvalidValue);
   for (StreamWs& e : g_stream_ws)
     if (e.st == st) {
       e = StreamWs{};
-      if (!ptr) return 0;
       break;
     }
-  if (!ptr) return 0;
+  if (!ptr && max_ctas <= 0) return 0;
   for (StreamWs& e : g_stream_ws)
     if (!e.st) {
       e.st = st;
       e.w.ws = static_cast<float*>(ptr);
-      e.w.bytes = static_cast<size_t>(bytes);
+      e.w.bytes = ptr ? static_cast<size_t>(bytes) : 0;
+      e.max_ctas = std::max(0, max_ctas);
       return 0;
     }
   return static_cast<int>(cudaErrorMemoryAllocation);

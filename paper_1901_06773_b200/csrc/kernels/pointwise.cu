@@ -10,6 +10,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstdint>
 
@@ -93,6 +95,8 @@ struct BnArgs {
                          // phase 1 sums these instead of reading x
   BnWs w;
   long long* trace;      // debug: globaltimer stamps per block (accudnn_bn_trace)
+  int l2_keep;           // phase-1 reads of the tensors phase 3 re-reads: L2 evict_last
+  int l2_last;           // phase-3 (last) reads: L2 evict_first
 };
 long long* g_bn_trace = nullptr;
 __device__ __forceinline__ long long bn_gtimer() {
@@ -105,6 +109,25 @@ __device__ __forceinline__ long long bn_gtimer() {
     if (a.trace && threadIdx.x == 0)                                                    \
       a.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (i)] = bn_gtimer();           \
   } while (0)
+
+// 16-byte read-only loads with an L2 eviction-priority policy
+__device__ __forceinline__ uint64_t l2_policy(int prio) {  // 0 normal, 1 last, 2 first
+  uint64_t p;
+  if (prio == 1)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (prio == 2)
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_pol(const float* ptr, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(ptr), "l"(pol));
+  return v;
+}
 
 // grid-wide barrier (all blocks co-resident: cooperative launch):
 // counters[0] arrivals, counters[1] generation.  (Measured: one barrier over
@@ -224,16 +247,19 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
         a1[3] += q.w;
       }
   } else if (c_ok) {
+    // x (and dy) are read again in phase 3: keep them in L2 ahead of the
+    // shortcut, which phase 3 does not re-read when the mask is in smem
+    const uint64_t p_keep = l2_policy(a.l2_keep ? 1 : 0);
+    const uint64_t p_skip = l2_policy(a.l2_keep ? (use_mask ? 2 : 1) : 0);
     long long r = r_begin + lane_r;
     int kk = 0;
     for (; r + 3 * step < r_end; r += 4 * step, kk += 4) {  // 4 rows in flight
       float4 v[4], d[4], sk[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r + u * step) * C + c));
-        if (MODE == 1) d[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r + u * step) * C + c));
-        if (MODE == 1 && SKIP)
-          sk[u] = __ldg(reinterpret_cast<const float4*>(a.skip + (r + u * step) * C + c));
+        v[u] = ld_pol(a.x + (r + u * step) * C + c, p_keep);
+        if (MODE == 1) d[u] = ld_pol(a.dy + (r + u * step) * C + c, p_keep);
+        if (MODE == 1 && SKIP) sk[u] = ld_pol(a.skip + (r + u * step) * C + c, p_skip);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -241,10 +267,9 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
                   consume(v[u], MODE == 1 ? d[u] : v[u], (MODE == 1 && SKIP) ? sk[u] : v[u]));
     }
     for (; r < r_end; r += step, ++kk) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
-      const float4 d = MODE == 1 ? __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)) : v;
-      const float4 sk =
-          (MODE == 1 && SKIP) ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v;
+      const float4 v = ld_pol(a.x + r * C + c, p_keep);
+      const float4 d = MODE == 1 ? ld_pol(a.dy + r * C + c, p_keep) : v;
+      const float4 sk = (MODE == 1 && SKIP) ? ld_pol(a.skip + r * C + c, p_skip) : v;
       keep_mask(kk, consume(v, d, sk));
     }
   }
@@ -421,23 +446,24 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       }
       return v;
     };
-    // rows in reverse: the lines read last in phase 1 are the likeliest L2 hits
+    // rows in reverse: the lines read last in phase 1 are the likeliest L2 hits;
+    // last reads of this step are evict_first
+    const uint64_t p_last = l2_policy(a.l2_last ? 2 : 0);
     long long r = r_hi;
     for (; r - 3 * step >= r_begin; r -= 4 * step) {
       float4 v[4], kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        v[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r - u * step) * C + c));
-        kv[u] = SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + (r - u * step) * C + c)) : v[u];
+        v[u] = ld_pol(a.x + (r - u * step) * C + c, p_last);
+        kv[u] = SKIP ? ld_pol(a.skip + (r - u * step) * C + c, p_last) : v[u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         *reinterpret_cast<float4*>(a.y + (r - u * step) * C + c) = f(v[u], kv[u]);
     }
     for (; r >= r_begin; r -= step) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
-      *reinterpret_cast<float4*>(a.y + r * C + c) =
-          f(v, SKIP ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : v);
+      const float4 v = ld_pol(a.x + r * C + c, p_last);
+      *reinterpret_cast<float4*>(a.y + r * C + c) = f(v, SKIP ? ld_pol(a.skip + r * C + c, p_last) : v);
     }
     BN_STAMP(4);
   } else {
@@ -482,26 +508,24 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       put(a.dx, o, a.dx_beta);
       if (SKIP) put(a.dskip, gg, a.dskip_beta);  // d(shortcut) = masked dy
     };
+    const uint64_t p_last = l2_policy(a.l2_last ? 2 : 0);
     long long r = r_hi;  // reverse order, as above
     int kk = static_cast<int>((r_hi - first_row) / step);
     for (; r - 3 * step >= r_begin; r -= 4 * step, kk -= 4) {
       float4 xv[4], dv[4], kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        xv[u] = __ldg(reinterpret_cast<const float4*>(a.x + (r - u * step) * C + c));
-        dv[u] = __ldg(reinterpret_cast<const float4*>(a.dy + (r - u * step) * C + c));
-        kv[u] = (SKIP && !use_mask)
-                    ? __ldg(reinterpret_cast<const float4*>(a.skip + (r - u * step) * C + c))
-                    : xv[u];
+        xv[u] = ld_pol(a.x + (r - u * step) * C + c, p_last);
+        dv[u] = ld_pol(a.dy + (r - u * step) * C + c, p_last);
+        kv[u] = (SKIP && !use_mask) ? ld_pol(a.skip + (r - u * step) * C + c, p_last) : xv[u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) f(xv[u], dv[u], kv[u], r - u * step, kk - u);
     }
     for (; r >= r_begin; r -= step, --kk) {
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + r * C + c));
-      f(xv, __ldg(reinterpret_cast<const float4*>(a.dy + r * C + c)),
-        (SKIP && !use_mask) ? __ldg(reinterpret_cast<const float4*>(a.skip + r * C + c)) : xv, r,
-        kk);
+      const float4 xv = ld_pol(a.x + r * C + c, p_last);
+      f(xv, ld_pol(a.dy + r * C + c, p_last),
+        (SKIP && !use_mask) ? ld_pol(a.skip + r * C + c, p_last) : xv, r, kk);
     }
     BN_STAMP(4);
   }
@@ -516,6 +540,19 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
 //    early-stage layers that need every SM streaming.
 template <int MODE, bool SKIP>
 int bn_launch(BnArgs a, cudaStream_t st) {
+  // L2 eviction priorities (ACCUDNN_BN_L2HINTS: 0 off, 1 auto, 3 always,
+  // 4 auto without phase-3 hints on large layers).  Measured per shape
+  // (tools/bn_bench.py): evict_last on the re-read tensors pays while they
+  // fit in about half the L2 and costs 3-5% above that
+  static int hints = -1;
+  if (hints < 0) {
+    const char* e = std::getenv("ACCUDNN_BN_L2HINTS");
+    hints = e ? std::atoi(e) : 1;
+  }
+  const double reread = 4.0 * static_cast<double>(a.M) * a.C * (MODE == 1 ? 2 : 1);
+  const bool fits = reread <= (MODE == 1 ? 72.0 : 48.0) * (1 << 20);
+  a.l2_keep = hints == 3 || ((hints == 1 || hints == 4) && fits);
+  a.l2_last = hints == 3 || hints == 1 || (hints == 4 && fits);
   static int occ = 0;
   if (!occ) {
     if (MODE == 1 && SKIP)

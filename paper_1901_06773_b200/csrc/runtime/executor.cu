@@ -167,7 +167,8 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   // the side stream's weight gradients get their own share of it
   size_t side_ws = 0;
   if (cfg.wgrad_stream && conv_ws) {
-    side_ws = (conv_ws / 2) & ~static_cast<size_t>(4095);
+    const double f = std::min(0.9, std::max(0.1, cfg.side_ws_frac));
+    side_ws = static_cast<size_t>(static_cast<double>(conv_ws) * f) & ~static_cast<size_t>(4095);
     conv_ws -= side_ws;
   }
   if (cfg.budget) {
@@ -238,14 +239,18 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
          "pinned host store");
     }
 
-  ck(cudaStreamCreateWithFlags(&I.compute, cudaStreamNonBlocking), "stream");
+  int prio_lo = 0, prio_hi = 0;
+  ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
+  if (!cfg.stream_priority) prio_lo = prio_hi = 0;
+  ck(cudaStreamCreateWithPriority(&I.compute, cudaStreamNonBlocking, prio_hi), "stream");
   ck(cudaStreamCreateWithFlags(&I.d2h, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.h2d, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.comm_stream, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.input_stream, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&I.side, cudaStreamNonBlocking), "stream");
-  if (I.side_ws)
-    ckl(accudnn_conv_set_stream_workspace(I.side, I.side_ws, side_ws), "side workspace");
+  ck(cudaStreamCreateWithPriority(&I.side, cudaStreamNonBlocking, prio_lo), "stream");
+  if (I.side_ws || cfg.side_ctas > 0)
+    ckl(accudnn_conv_set_stream_workspace(I.side, I.side_ws, side_ws, cfg.side_ctas),
+        "side workspace");
   ck(cudaEventCreateWithFlags(&I.layout_done, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&I.input_ready, cudaEventDisableTiming), "event");
   auto mk = [](std::vector<cudaEvent_t>& v, size_t cnt, bool timing) {
@@ -289,7 +294,7 @@ Executor::~Executor() {
   Impl& I = *impl_;
   if (I.graph) cudaGraphExecDestroy(I.graph);
   if (I.comm) ncclCommDestroy(I.comm);
-  if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0);
+  if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0, 0);
   for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
                   &I.bucket_ready, &I.fork_ev, &I.wg_done})
     for (cudaEvent_t e : *v)
@@ -746,7 +751,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture");
       kernel_launches_ = enqueue_iteration(true);
       ck(cudaStreamEndCapture(cs, &g), "end capture");
-      ck(cudaGraphInstantiate(&I.graph, g, 0), "instantiate");
+      ck(cudaGraphInstantiate(&I.graph, g,
+                              cfg_.stream_priority ? cudaGraphInstantiateFlagUseNodePriority : 0),
+         "instantiate");
       cudaGraphDestroy(g);
       I.graph_lr = lr;
       I.graph_update = update;

@@ -53,6 +53,14 @@ struct ExecConfig {
   // weight gradients are only needed by the all-reduce and the update.
   // Not used in profiled or autotuning (first) steps.
   int wgrad_stream = 1;
+  // the compute stream (critical path) at the highest stream priority, the
+  // weight-gradient stream at the lowest: pending CTAs of the critical path
+  // are dispatched first (graph nodes keep their priorities)
+  int stream_priority = 0;  // measured: 2333 -> 2256 img/s (the side stream starves), off
+  // persistent weight-gradient grids on the side stream use at most this
+  // many SMs (0 = all)
+  int side_ctas = 0;
+  double side_ws_frac = 0.5;  // share of the split-K workspace for the side stream
 };
 
 struct StepStats {

@@ -1,7 +1,9 @@
 """BN forward/backward kernels at ResNet-152 k=27 shapes: device time per
 launch (CUDA graph of 20 launches, so host launch cost is excluded) and
 achieved HBM-equivalent bandwidth (fwd: 2 passes over x + write y = 3S;
-bwd: x, dy twice + write dx = 5S).  Usage: bn_bench.py [k]"""
+bwd: x, dy twice + write dx = 5S; fused residual tail relu(bn(x)+skip):
+fwd 4S (x twice, skip, y), bwd 7S (x, dy twice, skip, dx, dskip)).
+Usage: bn_bench.py [k]"""
 import ctypes
 import sys
 
@@ -26,10 +28,22 @@ for hw, C in shapes:
     dx = torch.empty_like(x)
     g, b = torch.ones(C, device=dev), torch.zeros(C, device=dev)
     mean, inv = torch.empty(C, device=dev), torch.empty(C, device=dev)
+    skip = torch.randn(M, C, device=dev)
+    dsk = torch.empty_like(x)
     res = []
-    for mode in (0, 1):
+    for mode in (0, 1, 2, 3):
         def run():
-            if mode == 0:
+            if mode == 2:
+                lib.accudnn_bn_add_relu_fwd(P(x.data_ptr()), P(skip.data_ptr()), M, C, P(g.data_ptr()),
+                                            P(b.data_ptr()), 1e-5, P(y.data_ptr()), P(mean.data_ptr()),
+                                            P(inv.data_ptr()), None, None, 0.1, P(ws.data_ptr()),
+                                            P(s.cuda_stream))
+            elif mode == 3:
+                lib.accudnn_bn_add_relu_bwd(P(x.data_ptr()), P(skip.data_ptr()), P(dy.data_ptr()), M, C,
+                                            P(g.data_ptr()), P(b.data_ptr()), P(mean.data_ptr()),
+                                            P(inv.data_ptr()), P(dx.data_ptr()), 0, P(dsk.data_ptr()), 0,
+                                            None, None, P(ws.data_ptr()), P(s.cuda_stream))
+            elif mode == 0:
                 lib.accudnn_bn_fwd(P(x.data_ptr()), M, C, P(g.data_ptr()), P(b.data_ptr()), 1e-5, 1,
                                    P(y.data_ptr()), P(mean.data_ptr()), P(inv.data_ptr()), None, None,
                                    0.1, P(ws.data_ptr()), P(s.cuda_stream))
@@ -53,9 +67,10 @@ for hw, C in shapes:
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / 20 * 1e3
         S = M * C * 4
-        res.append((us, (3 if mode == 0 else 5) * S / us / 1e3))
+        res.append((us, (3, 5, 4, 7)[mode] * S / us / 1e3))
     print(f"M={M:7d} C={C:5d} S={M*C*4/1e6:6.1f}MB  fwd {res[0][0]:7.1f} us ({res[0][1]:6.0f} GB/s)  "
-          f"bwd {res[1][0]:7.1f} us ({res[1][1]:6.0f} GB/s)", flush=True)
+          f"bwd {res[1][0]:7.1f} us ({res[1][1]:6.0f} GB/s)  tail fwd {res[2][0]:7.1f} us "
+          f"({res[2][1]:6.0f} GB/s)  tail bwd {res[3][0]:7.1f} us ({res[3][1]:6.0f} GB/s)", flush=True)
 
 # floor of a trivial kernel in the same graph setting
 x = torch.randn(1024, device=dev)
