@@ -599,6 +599,7 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     }
   }
 
+  const bool overlap_update = update && cfg_.overlap_update;
   auto enqueue_iteration = [&](bool capture) {
     int launches = 0;
     if (host_inputs && !capture) {
@@ -683,18 +684,28 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
            "offload");
         ck(cudaEventRecord(I.d2h_done[static_cast<size_t>(t)], I.d2h), "record");
       }
-      // data parallel: all-reduce completed gradient buckets while the
-      // backward continues
-      if (I.comm && !fwd) {
+      // completed gradient buckets (every op whose parameters lie in the
+      // prefix finished its backward on both streams): all-reduce them (data
+      // parallel) and apply their update while the backward continues
+      if ((I.comm || overlap_update) && !fwd) {
         const long long ready = prefix_after_step[static_cast<size_t>(s)];
         if (ready - reduced >= bucket || (s == 2 * n && ready > reduced)) {
           ck(cudaStreamWaitEvent(I.comm_stream, I.step_done[static_cast<size_t>(s)], 0), "wait");
           if (last_wg > 0)
             ck(cudaStreamWaitEvent(I.comm_stream, I.wg_done[static_cast<size_t>(last_wg)], 0), "wait");
-          ckn(ncclAllReduce(I.grads + reduced, I.grads + reduced,
-                            static_cast<size_t>(ready - reduced), ncclFloat, ncclSum, I.comm,
-                            I.comm_stream),
-              "ncclAllReduce");
+          if (I.comm)
+            ckn(ncclAllReduce(I.grads + reduced, I.grads + reduced,
+                              static_cast<size_t>(ready - reduced), ncclFloat, ncclSum, I.comm,
+                              I.comm_stream),
+                "ncclAllReduce");
+          if (overlap_update) {
+            ckl(accudnn_sgd_update(I.params + reduced, I.grads + reduced, I.momentum_buf + reduced,
+                                   ready - reduced, lr, cfg_.momentum, cfg_.weight_decay,
+                                   1.0f / static_cast<float>(I.world), I.first_step ? 1 : 0,
+                                   static_cast<void*>(I.comm_stream)),
+                "sgd");
+            ++launches;
+          }
           reduced = ready;
           comm_used = true;
         }
@@ -715,10 +726,11 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       ck(cudaEventRecord(I.step_done[2 * n + 1], I.h2d), "record");
       ck(cudaStreamWaitEvent(cs, I.step_done[2 * n + 1], 0), "wait");
     }
-    if (update) {
-      ckl(accudnn_sgd_update(I.params, I.grads, I.momentum_buf, net.n_params, lr,
-                             cfg_.momentum, cfg_.weight_decay, 1.0f / static_cast<float>(I.world),
-                             I.first_step ? 1 : 0, csv),
+    const long long updated = overlap_update ? reduced : 0;
+    if (update && updated < net.n_params) {
+      ckl(accudnn_sgd_update(I.params + updated, I.grads + updated, I.momentum_buf + updated,
+                             net.n_params - updated, lr, cfg_.momentum, cfg_.weight_decay,
+                             1.0f / static_cast<float>(I.world), I.first_step ? 1 : 0, csv),
           "sgd");
       ++launches;
     }

@@ -231,3 +231,25 @@ def test_wgrad_side_stream_matches_inline(cuda_dev, mode):
         assert la == lb == lc, (it, la, lb, lc)
     assert np.array_equal(a.get_params(), b.get_params())
     assert np.array_equal(a.get_params(), c.get_params())
+
+
+def test_bucketed_overlapped_update_matches_single_update(cuda_dev):
+    """per-bucket SGD updates on the communication stream during the backward
+    (ACCUDNN_OVERLAP_UPDATE=1) equal the single update after it, bit for bit."""
+    arch, image, classes, k = "resnet50", 64, 8, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=11)
+    a = trainer.Executor(arch, image, classes, k=k)
+    os.environ["ACCUDNN_OVERLAP_UPDATE"] = "1"
+    try:
+        b = trainer.Executor(arch, image, classes, k=k)
+    finally:
+        del os.environ["ACCUDNN_OVERLAP_UPDATE"]
+    for e in (a, b):
+        e.set_params(params)
+    b.set_graph(True)
+    a.set_graph(True)
+    for it in range(4):
+        x, y = data(k, image, classes, seed=60 + it)
+        assert a.step(x, y, lr=0.05)["loss"] == b.step(x, y, lr=0.05)["loss"], it
+    assert np.array_equal(a.get_params(), b.get_params())
