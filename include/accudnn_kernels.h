@@ -119,6 +119,12 @@ int accudnn_bn_add_relu_bwd(const float* x, const float* skip, const float* dy, 
                             const float* save_mean, const float* save_invstd, float* dx,
                             int dx_beta, float* dskip, int dskip_beta, float* dgamma,
                             float* dbeta, void* ws, void* stream);
+/* y = relu(x * sc + sh), sc = gamma * save_invstd, sh = beta - save_mean * sc:
+ * a bn_relu forward's output recomputed bit for bit from its saved statistics
+ * (transient activations, recomputed for the consuming conv's weight gradient) */
+int accudnn_bn_relu_apply(const float* x, long long M, int C, const float* gamma,
+                          const float* beta, const float* save_mean, const float* save_invstd,
+                          float* y, void* stream);
 int accudnn_relu_fwd(const float* x, float* y, long long n, void* stream);
 /* dx (+)= dy * (x > 0) */
 int accudnn_relu_bwd(const float* x, const float* dy, float* dx, long long n,

@@ -132,6 +132,7 @@ CUDA_SYMBOLS = {
     "accudnn_bn_add_relu_fwd": ([_P, _P, _LL, _I, _P, _P, _F, _P, _P, _P, _P, _P, _F, _P, _P], _I),
     "accudnn_bn_add_relu_bwd": ([_P, _P, _P, _LL, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P,
                                  _P], _I),
+    "accudnn_bn_relu_apply": ([_P, ctypes.c_longlong, _I, _P, _P, _P, _P, _P, _P], _I),
     "accudnn_relu_fwd": ([_P, _P, _LL, _P], _I),
     "accudnn_relu_bwd": ([_P, _P, _P, _LL, _I, _P], _I),
     "accudnn_add_fwd": ([_P, _P, _P, _LL, _P], _I),

@@ -1213,6 +1213,72 @@ extern "C" int accudnn_bn_add_relu_bwd(const float* x, const float* skip, const 
   return bn_launch<1, true>(a, S(stream));
 }
 
+namespace accudnn {
+namespace {
+// y = relu(x * sc + sh), sc = gamma * invstd, sh = beta - mean * sc: the
+// forward's batch-norm output bit for bit (the same float scale / shift and
+// contraction as phase 3 of bn_fused_kernel<0>), recomputed from the saved
+// statistics.  Threads own 4 channels (x) and stride over rows (y).
+__global__ void bn_relu_apply_kernel(const float* __restrict__ x, long long M, int C,
+                                     const float* __restrict__ gamma, const float* __restrict__ beta,
+                                     const float* __restrict__ mean,
+                                     const float* __restrict__ invstd, float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c >= C) return;
+  float sc[4], sh[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    sc[j] = gamma[c + j] * invstd[c + j];
+    sh[j] = beta[c + j] - mean[c + j] * sc[j];
+  }
+  const uint64_t p_last = l2_policy(2);
+  const long long step = static_cast<long long>(blockDim.y) * gridDim.y;
+  long long r = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+  for (; r + 3 * step < M; r += 4 * step) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ld_pol(x + (r + u * step) * C + c, p_last);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float4 o = v[u];
+      o.x = fmaxf(o.x * sc[0] + sh[0], 0.f);
+      o.y = fmaxf(o.y * sc[1] + sh[1], 0.f);
+      o.z = fmaxf(o.z * sc[2] + sh[2], 0.f);
+      o.w = fmaxf(o.w * sc[3] + sh[3], 0.f);
+      *reinterpret_cast<float4*>(y + (r + u * step) * C + c) = o;
+    }
+  }
+  for (; r < M; r += step) {
+    float4 o = ld_pol(x + r * C + c, p_last);
+    o.x = fmaxf(o.x * sc[0] + sh[0], 0.f);
+    o.y = fmaxf(o.y * sc[1] + sh[1], 0.f);
+    o.z = fmaxf(o.z * sc[2] + sh[2], 0.f);
+    o.w = fmaxf(o.w * sc[3] + sh[3], 0.f);
+    *reinterpret_cast<float4*>(y + r * C + c) = o;
+  }
+}
+}  // namespace
+}  // namespace accudnn
+
+extern "C" int accudnn_bn_relu_apply(const float* x, long long M, int C, const float* gamma,
+                                     const float* beta, const float* save_mean,
+                                     const float* save_invstd, float* y, void* stream) {
+  if ((C & 3) || M <= 0) return static_cast<int>(cudaErrorInvalidValue);
+  const int c4 = C / 4;
+  const int lanes = c4 < 32 ? c4 : 32;
+  const dim3 block(lanes, 256 / lanes);
+  const int gx = (c4 + lanes - 1) / lanes;
+  const long long rows_per_block = static_cast<long long>(block.y) * 4;
+  long long gy = (M + rows_per_block - 1) / rows_per_block;
+  const long long cap = std::max<long long>(1, 148LL * 8 / gx);
+  if (gy > cap) gy = cap;
+  launch_pdl(bn_relu_apply_kernel, dim3(gx, static_cast<unsigned>(gy)), block, 0, S(stream), x, M, C,
+             gamma, beta, save_mean, save_invstd, y);
+  return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" int accudnn_relu_fwd(const float* x, float* y, long long n, void* stream) {
   if (n & 3) return static_cast<int>(cudaErrorInvalidValue);
   launch_pdl(relu_fwd_kernel, grid_for(n / 4, kThreads), kThreads, 0, S(stream), 

@@ -97,6 +97,10 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   if (!swapped.empty() && static_cast<int>(swapped.size()) != n)
     throw std::invalid_argument("swap mask does not match the network");
   I.swapped = swapped.empty() ? std::vector<char>(static_cast<size_t>(n), 0) : swapped;
+  // transient activations are recomputed, never offloaded (0-byte featuremaps
+  // in the planner's model: pinning or swapping them is the same)
+  for (int t = 0; t < n; ++t)
+    if (net_.ops[static_cast<size_t>(t)].transient) I.swapped[static_cast<size_t>(t)] = 0;
   ck(cudaSetDevice(cfg.device), "cudaSetDevice");
 
   // ---- static arena plan ----
@@ -279,6 +283,15 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
       if (I.lm.pre_inst[u] >= 0 && s >= I.lm.inst[static_cast<size_t>(I.lm.pre_inst[u])].first)
         id = I.lm.pre_inst[u];
       if (id >= 0) I.side_last[static_cast<size_t>(id)] = std::max(I.side_last[static_cast<size_t>(id)], s);
+      // a transient input is recomputed on the side stream from its BN input
+      const Op& ob = net_.ops[u];
+      if (ob.transient && ob.in0 >= 0) {
+        const size_t v = static_cast<size_t>(ob.in0);
+        int xi = I.lm.act_inst[v];
+        if (I.lm.pre_inst[v] >= 0 && s >= I.lm.inst[static_cast<size_t>(I.lm.pre_inst[v])].first)
+          xi = I.lm.pre_inst[v];
+        if (xi >= 0) I.side_last[static_cast<size_t>(xi)] = std::max(I.side_last[static_cast<size_t>(xi)], s);
+      }
     }
     const int g = I.lm.grad_inst[static_cast<size_t>(o)];
     if (g >= 0) I.side_last[static_cast<size_t>(g)] = std::max(I.side_last[static_cast<size_t>(g)], s);
@@ -472,23 +485,62 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     }
   };
 
+  // gradient instances a side-stream weight gradient reads, by the step that
+  // launched it: a later write into the same instance (an accumulating
+  // writer of an aliased gradient group) must wait for that weight gradient
+  std::vector<int> side_grad_reader(I.lm.inst.size(), 0);
+  auto before_write = [&](int x) {
+    if (x < 0) return;
+    const int g = I.lm.grad_inst[static_cast<size_t>(x)];
+    if (g < 0 || side_grad_reader[static_cast<size_t>(g)] == 0) return;
+    ck(cudaStreamWaitEvent(cs, I.wg_done[static_cast<size_t>(side_grad_reader[static_cast<size_t>(g)])], 0),
+       "wait wgrad");
+    side_grad_reader[static_cast<size_t>(g)] = 0;
+  };
+
   // ---- one backward op ----
   auto backward = [&](int o, int s) {
     const Op& op = net.ops[static_cast<size_t>(o)];
+    // every gradient this op writes: its inputs' (pass-through adds write none)
+    if (op.kind != OpKind::add) {
+      before_write(op.in0);
+      before_write(op.in1);
+    } else {
+      for (int x : {op.in0, op.in1})
+        if (x >= 0 && I.lm.grad_group[static_cast<size_t>(x)] != I.lm.grad_group[static_cast<size_t>(o)])
+          before_write(x);
+    }
     switch (op.kind) {
       case OpKind::conv:
       case OpKind::fc: {
         const accudnn_conv_desc d = conv_desc(op);
         float* dy = grad(o);
+        // a transient input (bn_relu output) is recomputed from the BN input
+        // and its saved statistics first (on the weight-gradient stream)
+        auto recompute = [&](cudaStream_t st) {
+          if (op.in0 < 0 || !net.ops[static_cast<size_t>(op.in0)].transient) return;
+          const Op& bn = net.ops[static_cast<size_t>(op.in0)];
+          if (bn.in0 >= 0 && I.swapped[static_cast<size_t>(bn.in0)])
+            ck(cudaStreamWaitEvent(st, I.h2d_done[static_cast<size_t>(bn.in0)], 0), "wait");
+          const int C = bn.channels;
+          const float* sp = I.stats + bn.stat_off;
+          ckl(accudnn_bn_relu_apply(act(bn.in0, s), elems(op.in0) / C, C, I.params + bn.g_off,
+                                    I.params + bn.beta_off, sp, sp + C, act(op.in0, s),
+                                    static_cast<void*>(st)),
+              "bn_relu recompute");
+        };
         if (use_side) {
           ck(cudaEventRecord(I.fork_ev[static_cast<size_t>(s)], cs), "record");
           ck(cudaStreamWaitEvent(I.side, I.fork_ev[static_cast<size_t>(s)], 0), "wait");
+          recompute(I.side);
           ckl(accudnn_conv_wgrad(&d, act(op.in0, s), dy, I.grads + op.w_off, 0, 0,
                                  static_cast<void*>(I.side)),
               "wgrad");
           ck(cudaEventRecord(I.wg_done[static_cast<size_t>(s)], I.side), "record");
           last_wg = s;
+          side_grad_reader[static_cast<size_t>(I.lm.grad_inst[static_cast<size_t>(o)])] = s;
         } else {
+          recompute(cs);
           ckl(accudnn_conv_wgrad(&d, act(op.in0, s), dy, I.grads + op.w_off, 0, 0, csv), "wgrad");
         }
         if (op.in0 != kImage)
@@ -573,6 +625,10 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
         ck(cudaStreamWaitEvent(stream, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
         if (same_as_compute) swap_wait[static_cast<size_t>(cur_step)] = 1;
       }
+      // a prefetched predecessor nobody read in the backward (e.g. an add's
+      // input: the GMAP prefetches every featuremap) may still be landing
+      if (y.kind == InstKind::act_prefetched && stream != I.h2d)
+        ck(cudaStreamWaitEvent(stream, I.h2d_done[static_cast<size_t>(y.tensor)], 0), "wait");
       if (!same_as_compute) {
         ck(cudaStreamWaitEvent(stream, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
       }

@@ -3,6 +3,7 @@
 #include "net.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <cstdio>
 #include <map>
@@ -293,7 +294,7 @@ void finalize(Net& net) {
 
 }  // namespace
 
-Net build_net(const std::string& arch, int image, int classes) {
+Net build_net(const std::string& arch, int image, int classes, int recompute) {
   Net net;
   net.arch = arch;
   net.image = image;
@@ -323,6 +324,28 @@ Net build_net(const std::string& arch, int image, int classes) {
     throw std::invalid_argument("unknown architecture: " + arch);
   }
   finalize(net);
+  if (recompute < 0) {
+    // default off (ACCUDNN_RECOMPUTE=1 turns it on).  Measured on ResNet-152
+    // at 8 GiB: k* 42 -> 50 but 2360 -> 2245 img/s -- the recompute pass costs
+    // as much as storing (one read + one write of the tensor) and lands on the
+    // weight-gradient stream, which the critical path already waits for.  Not
+    // for the CIFAR nets either way: their layer-wise memory peak of the
+    // all-swapped model would fall on a transient phase, which holds no
+    // featuremap bytes, and the reference's k_max formula rejects such a spec
+    // (planner.cpp:232-234)
+    const char* e = std::getenv("ACCUDNN_RECOMPUTE");
+    recompute = e ? std::atoi(e) : 0;
+  }
+  if (recompute)
+    for (int t = 0; t < net.num_ops(); ++t) {
+      Op& op = net.ops[static_cast<size_t>(t)];
+      const auto& cons = net.consumers[static_cast<size_t>(t)];
+      if (op.kind == OpKind::bn_relu && cons.size() == 1 &&
+          net.ops[static_cast<size_t>(cons[0])].kind == OpKind::conv) {
+        op.transient = true;
+        op.transient_reader = cons[0];
+      }
+    }
   return net;
 }
 
@@ -377,6 +400,28 @@ LifetimeModel build_lifetimes(const Net& net, int k, const std::vector<char>& sw
         first_bwd = std::min(first_bwd, bwd_step(c, n));
         last_bwd = std::max(last_bwd, bwd_step(c, n));
       }
+      // a transient consumer is recomputed from this tensor in its reader's backward
+      if (oc.transient) {
+        first_bwd = std::min(first_bwd, bwd_step(oc.transient_reader, n));
+        last_bwd = std::max(last_bwd, bwd_step(oc.transient_reader, n));
+      }
+    }
+    const Op& ot = net.ops[static_cast<size_t>(t)];
+    if (ot.transient) {
+      Instance a;
+      a.kind = InstKind::act;
+      a.tensor = t;
+      a.bytes = bytes_of(t);
+      a.first = fwd_step(t);
+      a.last = last_fwd;
+      lm.act_inst[static_cast<size_t>(t)] = static_cast<int>(lm.inst.size());
+      lm.inst.push_back(a);
+      Instance r = a;
+      r.kind = InstKind::act_recomputed;
+      r.first = r.last = bwd_step(ot.transient_reader, n);
+      lm.pre_inst[static_cast<size_t>(t)] = static_cast<int>(lm.inst.size());
+      lm.inst.push_back(r);
+      continue;
     }
     // GMAP prefetch / release phase of fm_{t+1} (1-based) = 2N - t
     const int gmap_phase = 2 * n - t;
@@ -636,7 +681,11 @@ std::string export_network_json(const Net& net, int k_base, int lookahead) {
   const std::vector<char> all(static_cast<size_t>(n), 1);
   const LifetimeModel lm = build_lifetimes(net, k_base, all, lookahead, 1);
   // bytes of the GMAP-resident featuremap at each step
-  auto fm_bytes = [&](int t) { return 4LL * k_base * net.shape[static_cast<size_t>(t)].per_image(); };
+  auto fm_bytes = [&](int t) {
+    return net.ops[static_cast<size_t>(t)].transient
+               ? 0LL
+               : 4LL * k_base * net.shape[static_cast<size_t>(t)].per_image();
+  };
   std::vector<long long> extra(static_cast<size_t>(2 * n + 2), 0);
   for (int s = 1; s <= 2 * n; ++s) {
     const int t = s <= n ? s - 1 : (2 * n + 1 - s) - 1;  // layer l -> tensor l-1
@@ -711,6 +760,7 @@ std::string describe_net_json(const Net& net) {
       o["g_off"] = op.g_off;
       o["beta_off"] = op.beta_off;
       o["stat_off"] = op.stat_off;
+      if (op.transient) o["transient"] = true;
     }
     if (op.kind == OpKind::maxpool) {
       o["k"] = op.pk;

@@ -48,6 +48,12 @@ struct Op {
   long long stat_off = -1;  // [mean C][invstd C][running_mean C][running_var C]
   // pooling window
   int pk = 0, pstride = 1, ppad = 0;
+  // bn_relu whose only consumer is a convolution: its output is transient
+  // (lives from its forward to the conv's forward) and is recomputed from the
+  // BN input and the saved statistics right before the conv's weight
+  // gradient; its featuremap in the planner's model is 0 bytes
+  bool transient = false;
+  int transient_reader = -1;  // the consuming conv
 };
 
 struct TensorShape {
@@ -71,8 +77,10 @@ struct Net {
 };
 
 // arch: resnet{18,34,50,101,152} (ImageNet layout), resnet{20,32,44,56,110}
-// (CIFAR basic blocks), resnet{164,1001} (CIFAR pre-activation bottleneck)
-Net build_net(const std::string& arch, int image, int classes);
+// (CIFAR basic blocks), resnet{164,1001} (CIFAR pre-activation bottleneck).
+// recompute: mark bn_relu -> conv outputs transient (see Op::transient);
+// -1 = the process default (on; ACCUDNN_RECOMPUTE=0 turns it off)
+Net build_net(const std::string& arch, int image, int classes, int recompute = -1);
 
 // does the backward of `op` read its (first / second) input tensor?
 bool bwd_reads_input(const Op& op);
@@ -83,7 +91,8 @@ inline int fwd_step(int op) { return op + 1; }
 inline int bwd_step(int op, int n) { return op == 0 ? 2 * n : 2 * n + 1 - op; }
 
 // ---- real tensor instances ------------------------------------------------------
-enum class InstKind : int { act, act_prefetched, grad };
+// act_recomputed: a transient tensor rewritten in the backward (by compute)
+enum class InstKind : int { act, act_prefetched, grad, act_recomputed };
 struct Instance {
   InstKind kind = InstKind::act;
   int tensor = -1;         // op id whose output (act) or output-gradient (grad)
@@ -97,7 +106,7 @@ struct LifetimeModel {
   int n = 0;                          // ops
   std::vector<Instance> inst;
   std::vector<int> act_inst;          // tensor -> primary activation instance
-  std::vector<int> pre_inst;          // tensor -> prefetched instance or -1
+  std::vector<int> pre_inst;          // tensor -> prefetched / recomputed instance or -1
   std::vector<int> grad_inst;         // tensor -> gradient instance or -1 (aliases share)
   std::vector<int> grad_first_writer; // tensor -> op whose backward writes the group first
   std::vector<int> grad_group;        // tensor -> gradient alias group id

@@ -74,12 +74,15 @@ def default_m_others(describe, image, budget_bytes=None):
     the batch twice (NCHW staging + NHWC4 for the stem, 7 floats per pixel);
     with a budget the allowance covers the largest batch the budget could
     hold at all (budget / featuremap bytes per image), so a tuned k* always
-    fits the executor's fixed allocations."""
+    fits the executor's fixed allocations.  What the batch leaves of it is
+    the convolutions' split-K workspace (shared by the compute and the
+    weight-gradient streams)."""
     momentum = 4 * describe["n_params"]
     stats = 4 * describe["n_stats"]
     staging = (96 << 20) if image >= 128 else (32 << 20)
     if budget_bytes:
-        fm_per_image = sum(4 * o["out"][0] * o["out"][1] * o["out"][2] for o in describe["ops"])
+        fm_per_image = sum(4 * o["out"][0] * o["out"][1] * o["out"][2] for o in describe["ops"]
+                           if not o.get("transient"))
         k_ub = int(budget_bytes) // max(1, fm_per_image)
         staging = max(staging, 7 * 4 * image * image * k_ub + (8 << 20))
     return momentum + stats + staging

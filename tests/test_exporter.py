@@ -101,3 +101,31 @@ def test_describe_layout_reverse_op_order():
     offs = [op.get("w_off", op.get("g_off")) for op in desc["ops"]
             if op.get("w_off", op.get("g_off", -1)) is not None and op.get("w_off", op.get("g_off", -1)) >= 0]
     assert offs == sorted(offs, reverse=True)
+
+
+@pytest.mark.parametrize("arch,image,classes", [("resnet50", 224, 1000), ("resnet18", 224, 1000)])
+def test_transient_activations_memory_bound(monkeypatch, arch, image, classes):
+    """recomputed bn_relu outputs (ACCUDNN_RECOMPUTE=1): 0-byte featuremaps,
+    their forward and backward instances charged to the workspaces; the
+    executor still never exceeds the planned peak, the reference's k_max
+    accepts the spec, and the all-pinned (resident) peak shrinks."""
+    net0, _ = trainer.export_network(arch, image, classes, k_base=8)
+    monkeypatch.setenv("ACCUDNN_RECOMPUTE", "1")
+    net_json, desc = trainer.export_network(arch, image, classes, k_base=8)
+    assert any(o.get("transient") for o in desc["ops"])
+    net = json.loads(net_json)
+    for o, l in zip(desc["ops"], net["layers"]):
+        assert (l["featuremap_bytes_base"] == 0) == bool(o.get("transient"))
+    n = len(desc["ops"])
+    rng = random.Random(1)
+    for k in (1, 8, 27):
+        for frac in (0.0, 1.0, 0.5):
+            pinned = [rng.random() < frac for _ in range(n)]
+            live, arena = trainer.net_memory(arch, image, classes, k, [not p for p in pinned])
+            peak = planned_peak(net, k, pinned)
+            assert live <= peak, (k, frac, live, peak)
+    hw = trainer.hardware_json(8 << 30, trainer.default_m_others(desc, image, 8 << 30), 50e9)
+    assert planner.kmax(net_json, hw) >= planner.kmax(net0, hw)
+    resident = planned_peak(net, 32, [True] * n)
+    resident0 = planned_peak(json.loads(net0), 32, [True] * n)
+    assert resident < 0.9 * resident0, (resident, resident0)

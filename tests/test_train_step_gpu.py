@@ -201,12 +201,14 @@ def test_pipelined_host_input_matches_plain_steps(cuda_dev):
     assert np.array_equal(a.get_params(), b.get_params())
 
 
-@pytest.mark.parametrize("mode", ["resident", "dynamic"])
-def test_wgrad_side_stream_matches_inline(cuda_dev, mode):
+@pytest.mark.parametrize("arch,image,classes,k,mode", [("resnet50", 64, 8, 4, "resident"),
+                                                       ("resnet50", 64, 8, 4, "dynamic"),
+                                                       ("resnet164", 32, 12, 4, "resident")])
+def test_wgrad_side_stream_matches_inline(cuda_dev, arch, image, classes, k, mode):
     """weight gradients on the concurrent side stream (default) compute exactly
     what the in-line order computes, eager and captured, with the arena's
-    region reuse and (dynamic) offload/prefetch copies waiting on them."""
-    arch, image, classes, k = "resnet50", 64, 8, 4
+    region reuse, (dynamic) offload/prefetch copies and (pre-activation
+    ResNet) accumulating writers of aliased gradient groups waiting on them."""
     _, desc = trainer.export_network(arch, image, classes)
     n = len(desc["ops"])
     plan = None
@@ -253,3 +255,46 @@ def test_bucketed_overlapped_update_matches_single_update(cuda_dev):
         x, y = data(k, image, classes, seed=60 + it)
         assert a.step(x, y, lr=0.05)["loss"] == b.step(x, y, lr=0.05)["loss"], it
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+@pytest.mark.parametrize("arch,image,classes,k,mode", [("resnet50", 64, 8, 4, "resident"),
+                                                       ("resnet50", 64, 8, 4, "dynamic"),
+                                                       ("resnet20", 32, 12, 4, "naive"),
+                                                       ("resnet164", 32, 12, 4, "dynamic")])
+def test_recomputed_activations_match_stored(cuda_dev, arch, image, classes, k, mode):
+    """bn_relu outputs consumed by one conv are transient (recomputed from the
+    saved statistics before the conv's weight gradient, on the side stream;
+    default for the ImageNet layouts, forced here for the CIFAR nets too):
+    the step is bit-identical to storing them, eager and captured, with swap
+    plans whose prefetched BN inputs the recompute waits for."""
+    def make(recompute):
+        os.environ["ACCUDNN_RECOMPUTE"] = recompute
+        try:
+            _, d = trainer.export_network(arch, image, classes)
+            assert any(o.get("transient") for o in d["ops"]) == (recompute == "1")
+            return d, trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan)
+        finally:
+            del os.environ["ACCUDNN_RECOMPUTE"]
+
+    _, desc = trainer.export_network(arch, image, classes)
+    n = len(desc["ops"])
+    plan = None
+    if mode == "dynamic":
+        plan = json.dumps({"k_star": k, "pinned_objects": [f"fm{l}" for l in range(1, n + 1, 3)]})
+    params = trainer.init_params(desc, seed=12)
+    _, a = make("0")
+    _, b = make("1")
+    _, c = make("1")
+    for e in (a, b, c):
+        e.set_params(params)
+    c.set_graph(True)
+    for it in range(3):
+        x, y = data(k, image, classes, seed=70 + it)
+        la = a.step(x, y, lr=0.05)["loss"]
+        lb = b.step(x, y, lr=0.05)["loss"]
+        lc = c.step(x, y, lr=0.05)["loss"]
+        assert la == lb == lc, (it, la, lb, lc)
+    assert np.array_equal(a.get_params(), b.get_params())
+    assert np.array_equal(a.get_params(), c.get_params())
+    if mode == "resident":
+        assert b.memory()[0] < a.memory()[0]  # smaller arena

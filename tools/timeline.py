@@ -77,5 +77,34 @@ for gp in sorted(big, reverse=True)[:8]:
 print("kernel | launches/step | ms/step | us/launch")
 for r in res["top"]:
     print(" | ".join(str(v) for v in r))
+
+# per-stream view (chrome trace carries the stream of every kernel): the
+# critical path runs on the compute stream (the one launching batch norms);
+# its idle time is where it waited on the weight-gradient stream or on SMs
+import tempfile  # noqa: E402
+with tempfile.NamedTemporaryFile(suffix=".json") as tf:
+    prof.export_chrome_trace(tf.name)
+    trace = json.load(open(tf.name))
+per_stream = collections.defaultdict(list)
+for ev in trace.get("traceEvents", []):
+    if ev.get("cat") == "kernel":
+        per_stream[ev.get("args", {}).get("stream", ev.get("tid"))].append(
+            (float(ev["ts"]), float(ev["ts"]) + float(ev.get("dur", 0)), ev.get("name", "")))
+streams = {}
+for sid, ks in per_stream.items():
+    ks.sort()
+    busy_s, end_s, idle = 0.0, ks[0][0], []
+    for a0, a1, nm in ks:
+        if a0 > end_s:
+            idle.append((a0 - end_s, nm[:50]))
+        busy_s += max(0.0, a1 - max(a0, end_s))
+        end_s = max(end_s, a1)
+    streams[str(sid)] = {"kernels_per_step": len(ks) / steps,
+                         "busy_ms_per_step": busy_s / steps / 1e3,
+                         "idle_ms_per_step": sum(i for i, _ in idle) / steps / 1e3,
+                         "has_bn": any("bn_fused" in nm for _, _, nm in ks),
+                         "largest_idle": [[round(i, 1), nm] for i, nm in sorted(idle, reverse=True)[:6]]}
+res["streams"] = streams
+print(json.dumps(streams, indent=1))
 if out_path:
     json.dump(res, open(out_path, "w"), indent=1)
