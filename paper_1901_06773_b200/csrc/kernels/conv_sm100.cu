@@ -152,6 +152,58 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// CTA pair (cta_group::2) loads: the box lands in this CTA's shared memory
+// and completes its bytes on the pair leader's barrier (shared::cluster
+// address `bar_cl`)
+__device__ __forceinline__ void tma_2d_g2(const CUtensorMap* tm, uint32_t dst, uint32_t bar_cl,
+                                          int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_g2(const CUtensorMap* tm, uint32_t dst, uint32_t bar_cl,
+                                          int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d_g2(const CUtensorMap* tm, uint32_t dst, uint32_t bar_cl,
+                                          int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_im2col_g2(const CUtensorMap* tm, uint32_t dst, uint32_t bar_cl,
+                                              int c, int w, int h, int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cl), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
+      "h"(oh)
+      : "memory");
+}
+// shared::cluster address of the same shared-memory offset in cluster CTA 0
+__device__ __forceinline__ uint32_t mapa_cta0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cl(uint32_t bar_cl, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
+                   bar_cl),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -239,16 +291,25 @@ __device__ __forceinline__ long long out_row(const Prob& a, int m) {
 // units, loads that tile's whole B (every k-block, <= ~128 KB) into shared
 // memory once, and streams only A through the ring -- half the operand
 // traffic of a 128 x BN tile for short-K GEMMs (1x1 convolutions)
-template <int MODE, int BN, int STAGES, int CM, int BS>
+// G = 2 (CM 2, FWD / DGRAD): the pair runs 2-SM MMAs (tcgen05 cta_group::2,
+// 256 x BN tiles): each CTA stages its 128 rows of A and half of the B
+// columns, both CTAs' loads complete on the even CTA's barriers, whose MMA
+// warp issues for the pair; each CTA's TMEM holds its 128 rows x BN.  Per SM
+// and k-block that is 16 KB of A + BN/2 x 128 B of B written and read in
+// shared memory instead of 16 KB + BN x 128 B: the stage traffic, which bounds
+// the single-CTA k-block rate, halves on the B side
+template <int MODE, int BN, int STAGES, int CM, int BS, int G>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const Prob a) {
+  static_assert(G == 1 || (CM == 2 && BS == 0 && MODE != WGRAD), "2-SM tiles: FWD / DGRAD pairs");
   constexpr bool kAmn = (MODE == WGRAD);
   constexpr bool kBmn = (MODE != FWD);
   constexpr uint32_t kABytes = kBM * kBK * 4;
   constexpr uint32_t kBBytes = BN * kBK * 4;
-  constexpr uint32_t kStageBytes = BS ? kABytes : kABytes + kBBytes;  // ring stage
+  constexpr uint32_t kBLocal = kBBytes / G;  // this CTA's B bytes per stage
+  constexpr uint32_t kStageBytes = BS ? kABytes : kABytes + kBLocal;  // ring stage
   constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -294,11 +355,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], CM);
+      ptx::mbar_init(&empty[s], G == 2 ? 1 : CM);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], kEpiThreads);
+      ptx::mbar_init(&tempty[s], G == 2 ? 2 * (kEpiThreads / 32) : kEpiThreads);
     }
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
@@ -306,7 +367,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmB);
     if (a.tma_out) prefetch_tmap(&tmC);
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (G == 2)
+      ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else
+      ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
   if (CM > 1)
     cluster_sync_all();  // peers' barriers initialised before any multicast / remote arrive
@@ -380,9 +446,46 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sA = smem_base + stage * kStageBytes;
           const uint32_t sB = sA + kABytes;
           uint64_t* bar = &full[stage];
-          mbar_expect_tx(bar, kStageBytes);
+          uint32_t full_cl = 0;  // G = 2: the even CTA's barrier
+          if constexpr (G == 2) {
+            // the even CTA's producer expects both CTAs' bytes; the odd CTA's
+            // loads only complete bytes on it
+            full_cl = mapa_cta0(ptx::smem_u32(bar));
+            if (crank == 0) mbar_expect_tx(bar, 2 * kStageBytes);
+          } else {
+            mbar_expect_tx(bar, kStageBytes);
+          }
           const int kk = kb * kBK;
-          if constexpr (BS && MODE == FWD) {  // A only
+          if constexpr (G == 2 && MODE == FWD) {
+            if (a.a_tiled) {
+              tma_2d_g2(&tmA, sA, full_cl, kk, m0);
+            } else {
+              const int tap = kk / a.C, c0 = kk - tap * a.C;
+              const int r = tap / a.S, s = tap - r * a.S;
+              tma_im2col_g2(&tmA, sA, full_cl, c0, pj * a.stride - a.pad, pi * a.stride - a.pad, pn,
+                            static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            }
+            tma_2d_g2(&tmB, sB, full_cl, kk, n0 + static_cast<int>(crank) * (BN / 2));
+          } else if constexpr (G == 2 && MODE == DGRAD) {
+            const int t = kk / a.K, co0 = kk - t * a.K;
+            const int tr = t / a.Sc, ts = t - tr * a.Sc;
+            const int tap = (a.r0 - a.stride * tr) * a.S + (a.s0 - a.stride * ts);
+            if (a.a_tiled) {
+              tma_2d_g2(&tmA, sA, full_cl, co0, m0);
+            } else {
+              tma_im2col_g2(&tmA, sA, full_cl, co0, pj + a.lo_w, pi + a.lo_h, pn,
+                            static_cast<uint16_t>(ts), static_cast<uint16_t>(tr));
+            }
+            constexpr int kHalf = BN / 64;  // this CTA's 32-column atoms
+            const int b0 = static_cast<int>(crank) * kHalf;
+            if (a.b_packed) {
+              tma_4d_g2(&tmB, sB, full_cl, 0, co0, n0 / 32 + b0, tap);
+            } else {
+#pragma unroll
+              for (int b = 0; b < kHalf; ++b)
+                tma_3d_g2(&tmB, sB + b * 4096, full_cl, n0 + 32 * (b0 + b), tap, co0);
+            }
+          } else if constexpr (BS && MODE == FWD) {  // A only
             if (a.a_tiled) {
               tma_2d(&tmA, sA, bar, kk, m0);
             } else {
@@ -465,9 +568,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && (G == 1 || crank == 0)) {
       // ============================ MMA issuer ============================
-      constexpr uint32_t idesc = ptx::idesc_tf32(kBM, BN, kAmn, kBmn);
+      constexpr uint32_t idesc = ptx::idesc_tf32(kBM * G, BN, kAmn, kBmn);
       uint32_t kc = 0;
       int j = 0;  // units processed by this CTA
       if (BS && cid < a.units) ptx::mbar_wait(bfull, 0);
@@ -492,14 +595,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : ptx::smem_desc(sA + ks * 32, 16, 1024, 2);
             const uint64_t bd = kBmn ? ptx::smem_desc(sB + ks * 1024, 4096, 512, 1)
                                      : ptx::smem_desc(sB + ks * 32, 16, 1024, 2);
-            ptx::mma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+            if constexpr (G == 2)
+              ptx::mma_tf32_pair(d_tmem, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+            else
+              ptx::mma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
           }
-          if (CM > 1)
+          if (G == 2)
+            ptx::mma_commit_pair(&empty[stage], kMask);  // both CTAs' stages consumed
+          else if (CM > 1)
             mma_commit_mc(&empty[stage], kMask);  // the stage holds the peer's B half too
           else
             ptx::mma_commit(&empty[stage]);
         }
-        ptx::mma_commit(&tfull[acc]);
+        if (G == 2)
+          ptx::mma_commit_pair(&tfull[acc], kMask);  // both CTAs' accumulator rows
+        else
+          ptx::mma_commit(&tfull[acc]);
       }
     }
   } else {
@@ -539,7 +650,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_ld32(trow + c0, cur);
         if (ci + 1 >= nch) {  // accumulator drained: release it to the MMA warp
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[acc]);
+          if constexpr (G == 2) {  // one arrive per warp on the even CTA's barrier
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cl(mapa_cta0(ptx::smem_u32(&tempty[acc])));
+          } else {
+            ptx::mbar_arrive(&tempty[acc]);
+          }
         }
         const uint32_t sbuf = sbuf0 + (nchunk & 1) * 4096;
         if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
@@ -619,7 +735,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (nch == 0) {  // tile entirely past Ng (cannot happen with tiles_n = ceil(Ng/BN))
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&tempty[acc]);
+        if constexpr (G == 2) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cl(mapa_cta0(ptx::smem_u32(&tempty[acc])));
+        } else {
+          ptx::mbar_arrive(&tempty[acc]);
+        }
       }
       if (a.trace && threadIdx.x == 64 && j < 128) a.trace[blockIdx.x * 1024 + 513 + 2 * j] = clock64();
     }
@@ -633,7 +754,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<kTmemCols>(tmem);
+    if constexpr (G == 2)
+      ptx::tmem_dealloc_pair<kTmemCols>(tmem);
+    else
+      ptx::tmem_dealloc<kTmemCols>(tmem);
   }
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 770] = gtimer();
 }
@@ -871,15 +995,15 @@ int choose_splits(long long tiles, int kb_total, int bn, long long out_elems, in
   return best;
 }
 
-template <int MODE, int BN, int STAGES, int CM, int BS>
+template <int MODE, int BN, int STAGES, int CM, int BS, int G>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
              cudaStream_t st) {
   const size_t ring = BS ? STAGES * kBM * kBK * 4 + static_cast<size_t>(a.kb_total) * BN * kBK * 4
-                         : STAGES * (kBM + BN) * kBK * 4;
+                         : STAGES * (kBM + BN / G) * kBK * 4;
   const size_t smem = ring + 1024 + 1024 + 4 * 8192;
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS>,
+    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                227 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
@@ -904,7 +1028,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   cfg.attrs = attr;
   cfg.numAttrs = CM > 1 ? 2 : 1;
   cudaError_t e =
-      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS>, ta, tb, tc, a);
+      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
   if (a.stats) {
@@ -1071,17 +1195,22 @@ bool encode(const Call& c, int bn, int cm, CUtensorMap* ta, CUtensorMap* tb, Pro
                     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int MODE, int CM, int BS>
+template <int MODE, int CM, int BS, int G = 1>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
                 int bn, cudaStream_t st) {
   if (BS) {  // A-only ring of 4 x 16 KB; B lives in its own region
-    if (bn == 256) return launch_t<MODE, 256, 4, CM, BS>(ta, tb, tc, a, st);
-    if (bn == 128) return launch_t<MODE, 128, 4, CM, BS>(ta, tb, tc, a, st);
-    return launch_t<MODE, 64, 4, CM, BS>(ta, tb, tc, a, st);
+    if (bn == 256) return launch_t<MODE, 256, 4, CM, BS, 1>(ta, tb, tc, a, st);
+    if (bn == 128) return launch_t<MODE, 128, 4, CM, BS, 1>(ta, tb, tc, a, st);
+    return launch_t<MODE, 64, 4, CM, BS, 1>(ta, tb, tc, a, st);
   }
-  if (bn == 256) return launch_t<MODE, 256, 4, CM, BS>(ta, tb, tc, a, st);
-  if (bn == 128) return launch_t<MODE, 128, 6, CM, BS>(ta, tb, tc, a, st);
-  return launch_t<MODE, 64, 8, CM, BS>(ta, tb, tc, a, st);
+  if (G == 2) {  // 32 / 24 / 20 KB stages
+    if (bn == 256) return launch_t<MODE, 256, 6, CM, BS, G>(ta, tb, tc, a, st);
+    if (bn == 128) return launch_t<MODE, 128, 8, CM, BS, G>(ta, tb, tc, a, st);
+    return launch_t<MODE, 64, 8, CM, BS, G>(ta, tb, tc, a, st);
+  }
+  if (bn == 256) return launch_t<MODE, 256, 4, CM, BS, 1>(ta, tb, tc, a, st);
+  if (bn == 128) return launch_t<MODE, 128, 6, CM, BS, 1>(ta, tb, tc, a, st);
+  return launch_t<MODE, 64, 8, CM, BS, 1>(ta, tb, tc, a, st);
 }
 
 // -1: could not encode the tensor maps (not launched)
@@ -1092,7 +1221,8 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   if (cfg.bs && (c.mode == WGRAD || cfg.splits != 1 || cfg.cm != 1 ||
                  static_cast<size_t>(c.a.kb_total) * cfg.bn * kBK * 4 > kMaxBStat))
     cfg.bs = 0;
-  if (!encode(c, cfg.bn, cfg.cm, &ta, &tb, a)) return -1;
+  // cm 4: CTA pair running 2-SM MMAs (each CTA loads half of the B columns, like cm 2)
+  if (!encode(c, cfg.bn, cfg.cm > 1 ? 2 : 1, &ta, &tb, a)) return -1;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (a.Ng + cfg.bn - 1) / cfg.bn;
   a.splits = cfg.splits;
@@ -1122,12 +1252,14 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   if (cfg.bs && a.tiles_n > sm_count()) cfg.bs = 0;
   if (c.mode == FWD)
     return cfg.bs ? dispatch_bn<FWD, 1, 1>(ta, tb, tc, a, cfg.bn, st)
-                  : cfg.cm > 1 ? dispatch_bn<FWD, 2, 0>(ta, tb, tc, a, cfg.bn, st)
-                               : dispatch_bn<FWD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
+           : cfg.cm == 4 ? dispatch_bn<FWD, 2, 0, 2>(ta, tb, tc, a, cfg.bn, st)
+           : cfg.cm > 1  ? dispatch_bn<FWD, 2, 0>(ta, tb, tc, a, cfg.bn, st)
+                         : dispatch_bn<FWD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
   if (c.mode == DGRAD)
     return cfg.bs ? dispatch_bn<DGRAD, 1, 1>(ta, tb, tc, a, cfg.bn, st)
-                  : cfg.cm > 1 ? dispatch_bn<DGRAD, 2, 0>(ta, tb, tc, a, cfg.bn, st)
-                               : dispatch_bn<DGRAD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
+           : cfg.cm == 4 ? dispatch_bn<DGRAD, 2, 0, 2>(ta, tb, tc, a, cfg.bn, st)
+           : cfg.cm > 1  ? dispatch_bn<DGRAD, 2, 0>(ta, tb, tc, a, cfg.bn, st)
+                         : dispatch_bn<DGRAD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
   return dispatch_bn<WGRAD, 1, 0>(ta, tb, tc, a, cfg.bn, st);
 }
 
@@ -1164,11 +1296,10 @@ Cfg tune(const Call& c, cudaStream_t st) {
   cudaEventCreate(&e1);
   Cfg best = model_cfg(c);
   float best_ms = 1e30f;
-  // 0: plain, 1: 2-CTA multicast.  (2, B-stationary, is available through
-  // accudnn_conv_force_cfg but not tuned: measured no faster -- the k-block
-  // rate is bound by bytes in flight per SM x memory latency, not by B traffic)
-  for (int variant : {0, 1}) {
-   const int cm = variant == 1 ? 2 : 1;
+  // 0: plain, 1: 2-CTA multicast, 3: 2-SM MMA pair.  (2, B-stationary, is
+  // available through accudnn_conv_force_cfg but not tuned: measured no faster)
+  for (int variant : {0, 1, 3}) {
+   const int cm = variant == 1 ? 2 : variant == 3 ? 4 : 1;
    const int bs = variant == 2 ? 1 : 0;
    if (variant > 0 && c.mode == WGRAD) continue;
    for (int bn : {64, 128, 256}) {
@@ -1490,7 +1621,7 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     for (int& v : key) ok = ok && static_cast<bool>(ls >> v);
     ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
     if (!ok) continue;
-    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2)) cfg.cm = 1;
+    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4)) cfg.cm = 1;
     if (!(ls >> cfg.bs) || (cfg.bs != 0 && cfg.bs != 1)) cfg.bs = 0;
     if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;
     if (cfg.splits < 1) continue;

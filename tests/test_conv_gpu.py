@@ -63,15 +63,23 @@ def check(got, ref):
     assert (got - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-6
 
 
-@pytest.fixture(params=["tma", "tma_cluster2", "tma_bn64_split3", "tma_bstat", "cpasync"])
+@pytest.fixture(params=["tma", "tma_cluster2", "tma_pair", "tma_pair_bn256_split2", "tma_pair_bn64",
+                        "tma_bn64_split3", "tma_bstat", "cpasync"])
 def impl(request):
     """TMA kernel with the analytic config, with the B tile multicast across an
-    M-tile pair (cluster of 2), with narrow tiles + forced split-K, and the
-    cp.async kernel."""
+    M-tile pair (cluster of 2), as a CTA pair running 2-SM MMAs (256-row
+    tiles, each CTA holding half of B), with narrow tiles + forced split-K,
+    and the cp.async kernel."""
     lib = _native.cuda_lib()
     lib.accudnn_set_conv_impl(0 if request.param == "cpasync" else 1)
     if request.param == "tma_cluster2":
         lib.accudnn_conv_force_cfg(0, 0, 2)
+    elif request.param == "tma_pair":
+        lib.accudnn_conv_force_cfg(0, 0, 4)
+    elif request.param == "tma_pair_bn256_split2":
+        lib.accudnn_conv_force_cfg(256, 2, 4)
+    elif request.param == "tma_pair_bn64":
+        lib.accudnn_conv_force_cfg(64, 1, 4)
     elif request.param == "tma_bn64_split3":
         lib.accudnn_conv_force_cfg(64, 3, 1)
     elif request.param == "tma_bstat":  # B-stationary where the B tile fits, else analytic
@@ -214,6 +222,7 @@ def test_dgrad_strided_accumulate(cuda_dev, shape):
                                           ((8, 256, 14, 14, 1024, 1, 1, 0), (128, 0, 3)),
                                           ((27, 1024, 14, 14, 256, 1, 1, 0), (256, 4, 1)),
                                           ((4, 64, 28, 28, 64, 3, 1, 1), (0, 0, 2)),
+                                          ((5, 128, 14, 14, 256, 3, 1, 1), (0, 0, 4)),
                                           ((3, 96, 10, 10, 160, 3, 1, 1), (0, 0, 0))])
 def test_conv_fwd_stats_and_bn_from_stats(cuda_dev, shape, forced):
     """the forward conv's epilogue (or its split-K reduce) writes per-32-row
