@@ -89,6 +89,10 @@ struct Prob {
   int b_packed;        // DGRAD: B stage (BN/32 MN atoms) is one 4-D box; WGRAD 1x1: one 3-D box
 };
 
+// experiment switch (ACCUDNN_CONV_DRAIN=1): epilogues wait for their bulk
+// stores' global writes before the CTA exits (default: only for the reads)
+__constant__ int g_conv_drain = 0;
+
 // ---- TMA PTX -------------------------------------------------------------------
 __device__ __forceinline__ void tma_2d(const CUtensorMap* tm, uint32_t dst, uint64_t* bar, int c0,
                                        int c1) {
@@ -744,7 +748,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (a.trace && threadIdx.x == 64 && j < 128) a.trace[blockIdx.x * 1024 + 513 + 2 * j] = clock64();
     }
-    if (lane == 0) bulk_wait_all();  // bulk stores complete before the CTA retires
+    // the staging buffers must have been read before the CTA retires; the
+    // global writes themselves complete with the grid (no need to hold the SM)
+    if (lane == 0) {
+      if (g_conv_drain)
+        bulk_wait_all();
+      else
+        bulk_wait_read<0>();
+    }
   }
 
   ptx::tc_fence_before();
@@ -1338,6 +1349,13 @@ Cfg tune(const Call& c, cudaStream_t st) {
 Cfg g_force{0, 0, 0};  // test hook (accudnn_conv_force_cfg): fields > 0 override
 
 int run_call(const Call& c, cudaStream_t st) {
+  static const bool drain_set = [] {
+    const char* e = std::getenv("ACCUDNN_CONV_DRAIN");
+    const int v = e ? std::atoi(e) : 0;
+    if (v) cudaMemcpyToSymbol(g_conv_drain, &v, sizeof(v));
+    return true;
+  }();
+  (void)drain_set;
   if (g_force.bn > 0 || g_force.splits > 0 || g_force.cm > 0) {
     Cfg f = model_cfg(c);
     if (g_force.bn > 0 && bn_ok(c, g_force.bn)) f.bn = g_force.bn;
