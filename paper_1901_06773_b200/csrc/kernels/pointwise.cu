@@ -150,6 +150,15 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
   __syncthreads();
 }
 
+template <int MODE, bool SKIP>
+__device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c, int lane_r,
+                                          long long r_begin, long long r_end, long long step,
+                                          long long first_row, bool use_mask,
+                                          const float (&coef)[6][kBnGroup], const float (&mu)[4],
+                                          const float (&is)[4], const float (&ga)[4],
+                                          const float (&fsc)[4], const float (&fsh)[4],
+                                          const uint32_t* mask_smem);
+
 template <int MODE, bool CLUSTER, bool SKIP>
 __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) ? 2 : 1) bn_fused_kernel(const BnArgs a) {
   pdl_wait();
@@ -349,12 +358,22 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     if (threadIdx.x < V) {
       const int v = threadIdx.x;
       const int off = v < ch ? v : kBnGroup + (v - ch);
+      // all (<= 16) remote reads in flight at once (~200 cycles each), then
+      // summed in rank order
+      const unsigned nb = cluster.num_blocks();
+      float pv[16];
+#pragma unroll
+      for (unsigned r = 0; r < 16; ++r)
+        pv[r] = r < nb ? cluster.map_shared_rank(&cpart[0][0], r)[off] : 0.f;
       double t = 0.0;
-      for (unsigned r = 0; r < cluster.num_blocks(); ++r)  // rank order
-        t += static_cast<double>(cluster.map_shared_rank(&cpart[0][0], r)[off]);
+#pragma unroll
+      for (unsigned r = 0; r < 16; ++r)
+        if (r < nb) t += static_cast<double>(pv[r]);
       dsum[v] = t;
     }
-    cluster.sync();  // peers' partials are read before any block may exit
+    // peers' partials must be read before any block exits: arrive now, wait
+    // at the end of phase 3 (the barrier overlaps the normalisation pass)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   } else {
     grid_barrier(a.w.counters, gridDim.x * gridDim.y);
     // ---- phase 2: the group's Y slots, chunked over threads, fixed order ----
@@ -417,7 +436,22 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   __syncthreads();
 
   BN_STAMP(3);
-  // ---- phase 3: the block's rows again ----
+  bn_phase3<MODE, SKIP>(a, c_ok, lane_c, lane_r, r_begin, r_end, step, first_row, use_mask, coef,
+                        mu, is, ga, fsc, fsh, mask_smem);
+  if constexpr (CLUSTER) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ---- phase 3 of bn_fused_kernel: the block's rows again (normalise / dx) ----
+template <int MODE, bool SKIP>
+__device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c, int lane_r,
+                                          long long r_begin, long long r_end, long long step,
+                                          long long first_row, bool use_mask,
+                                          const float (&coef)[6][kBnGroup], const float (&mu)[4],
+                                          const float (&is)[4], const float (&ga)[4],
+                                          const float (&fsc)[4], const float (&fsh)[4],
+                                          const uint32_t* mask_smem) {
+  const long long C = a.C;
+  const int c = (blockIdx.x * a.lanes + lane_c) * 4;
   if (!c_ok) return;
   const int cl = lane_c * 4;
   // last row of this thread's phase-1 sequence r_begin + lane_r + k*step
