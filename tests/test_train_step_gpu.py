@@ -298,3 +298,28 @@ def test_recomputed_activations_match_stored(cuda_dev, arch, image, classes, k, 
     assert np.array_equal(a.get_params(), c.get_params())
     if mode == "resident":
         assert b.memory()[0] < a.memory()[0]  # smaller arena
+
+
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_bucketed_nccl_allreduce_path_single_rank(cuda_dev, overlap):
+    """the data-parallel step (NCCL all-reduce of ~25 MB gradient buckets on the
+    communication stream as backward completes them, joined with the weight-
+    gradient stream; optionally the per-bucket update after each all-reduce)
+    on a single-rank communicator equals the plain step bit for bit."""
+    arch, image, classes, k = "resnet50", 64, 8, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=13)
+    a = trainer.Executor(arch, image, classes, k=k)
+    os.environ["ACCUDNN_OVERLAP_UPDATE"] = overlap
+    try:
+        b = trainer.Executor(arch, image, classes, k=k)
+    finally:
+        del os.environ["ACCUDNN_OVERLAP_UPDATE"]
+    b.set_comm(trainer.nccl_unique_id(), 0, 1)
+    for e in (a, b):
+        e.set_params(params)
+        e.set_graph(True)
+    for it in range(3):
+        x, y = data(k, image, classes, seed=80 + it)
+        assert a.step(x, y, lr=0.05)["loss"] == b.step(x, y, lr=0.05)["loss"], it
+    assert np.array_equal(a.get_params(), b.get_params())
