@@ -323,3 +323,30 @@ def test_bucketed_nccl_allreduce_path_single_rank(cuda_dev, overlap):
         x, y = data(k, image, classes, seed=80 + it)
         assert a.step(x, y, lr=0.05)["loss"] == b.step(x, y, lr=0.05)["loss"], it
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+@pytest.mark.parametrize("arch,image,classes,mode,lookahead", [("resnet164", 32, 12, "naive", 3),
+                                                               ("resnet50", 64, 8, "dynamic", 2),
+                                                               ("resnet18", 64, 8, "dynamic", 1)])
+def test_side_stream_with_swapping_and_lookahead(cuda_dev, arch, image, classes, mode, lookahead):
+    """weight-gradient stream + offloads/prefetches with deeper prefetch
+    lookahead (regions reused across the three copy/compute streams): the
+    captured step equals the in-line eager step bit for bit."""
+    k = 4
+    _, desc = trainer.export_network(arch, image, classes)
+    n = len(desc["ops"])
+    plan = json.dumps({"k_star": k, "pinned_objects": [f"fm{l}" for l in range(2, n + 1, 4)]})
+    params = trainer.init_params(desc, seed=14)
+    os.environ["ACCUDNN_WGRAD_STREAM"] = "0"
+    try:
+        a = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan, lookahead=lookahead)
+    finally:
+        del os.environ["ACCUDNN_WGRAD_STREAM"]
+    b = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan, lookahead=lookahead)
+    a.set_params(params)
+    b.set_params(params)
+    b.set_graph(True)
+    for it in range(3):
+        x, y = data(k, image, classes, seed=90 + it)
+        assert a.step(x, y, lr=0.05)["loss"] == b.step(x, y, lr=0.05)["loss"], it
+    assert np.array_equal(a.get_params(), b.get_params())
