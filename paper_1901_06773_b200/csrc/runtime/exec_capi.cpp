@@ -95,6 +95,7 @@ int accudnn_exec_create(const char* arch, int image, int classes, const char* mo
     if (const char* e = std::getenv("ACCUDNN_STREAM_PRIO")) cfg.stream_priority = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_SIDE_CTAS")) cfg.side_ctas = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_OVERLAP_UPDATE")) cfg.overlap_update = std::atoi(e);
+    if (const char* e = std::getenv("ACCUDNN_CONV_BN_STATS")) cfg.conv_bn_stats = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_SIDE_WS_FRAC")) cfg.side_ws_frac = std::atof(e);
     const accudnn::Net net = accudnn::build_net(arch, image, classes);
     const int n = net.num_ops();
