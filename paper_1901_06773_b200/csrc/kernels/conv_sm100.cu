@@ -387,7 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t smem_base = ptx::smem_u32(smem);
   // everything above overlapped the previous kernel's tail (PDL)
   pdl_wait();
-  pdl_trigger();
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 769] = gtimer();
 
   if (warp == 0 || warp >= 6) {
@@ -617,6 +616,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_commit(&tfull[acc]);
       }
     }
+    // (PDL) the CTA's tensor-core work is issued: its successor may be
+    // scheduled while the last epilogue drains (it still waits for this grid)
+    if (lane == 0) pdl_trigger();
   } else {
     // ============================ epilogue ============================
     // Each warp drains its TMEM lane quadrant (32 rows) in 32-column chunks.

@@ -162,7 +162,6 @@ __device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c
 template <int MODE, bool CLUSTER, bool SKIP>
 __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) ? 2 : 1) bn_fused_kernel(const BnArgs a) {
   pdl_wait();
-  pdl_trigger();
   BN_STAMP(0);
   __shared__ float red[2][kBnThreads][4];
   __shared__ __align__(16) float cpart[2][kBnGroup];  // CLUSTER: this block's partial
@@ -436,6 +435,7 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   __syncthreads();
 
   BN_STAMP(3);
+  pdl_trigger();  // (PDL) the successor may be scheduled during the last pass
   bn_phase3<MODE, SKIP>(a, c_ok, lane_c, lane_r, r_begin, r_end, step, first_row, use_mask, coef,
                         mu, is, ga, fsc, fsh, mask_smem);
   if constexpr (CLUSTER) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
