@@ -350,3 +350,28 @@ def test_side_stream_with_swapping_and_lookahead(cuda_dev, arch, image, classes,
         x, y = data(k, image, classes, seed=90 + it)
         assert a.step(x, y, lr=0.05)["loss"] == b.step(x, y, lr=0.05)["loss"], it
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+def test_programmatic_dependent_launch_matches(cuda_dev):
+    """with programmatic dependent launch on (kernels scheduled while their
+    predecessor drains; every kernel waits before its first global access)
+    the captured step equals the plain one bit for bit."""
+    from paper_1901_06773_b200 import _native
+    lib = _native.cuda_lib()
+    arch, image, classes, k = "resnet50", 64, 8, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=15)
+    batches = [data(k, image, classes, seed=100 + i) for i in range(3)]
+    out = []
+    for pdl in (0, 1):
+        prev = lib.accudnn_set_pdl(pdl)
+        try:
+            e = trainer.Executor(arch, image, classes, k=k)
+            e.set_params(params)
+            e.set_graph(True)
+            losses = [e.step(x, y, lr=0.05)["loss"] for x, y in batches]
+            out.append((losses, e.get_params()))
+        finally:
+            lib.accudnn_set_pdl(prev)
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
