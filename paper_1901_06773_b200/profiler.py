@@ -4,7 +4,11 @@ perf-model fit (the paper's profiling stage).
 
   compute rows  minibatch,phase,layer_type,flops,time_s
                 one row per phase (1..2N) per sampled minibatch; time = CUDA
-                events around the phase's kernels on the compute stream
+                events around the phase's kernels on the compute stream of an
+                instrumented (eager, serial) step, scaled so that the phases sum
+                to the measured CUDA-graph step at that minibatch (the step the
+                executor actually runs: no launch gaps, weight gradients
+                overlapped) -- the phases keep their measured shares
   transfer rows minibatch,seq_no,bytes,time_s
                 one row per featuremap offload (GMAP sequence number of the
                 offload op) per sampled minibatch; time = CUDA events around
@@ -50,7 +54,8 @@ def phase_table(network_json):
     return out, int(net["k_base"])
 
 
-def profile_compute(arch, image, classes, network_json, ks, steps=2, seed=0):
+def profile_compute(arch, image, classes, network_json, ks, steps=2, seed=0, graph_steps=4,
+                    scale_to_graph=True):
     phases, k_base = phase_table(network_json)
     _, desc = trainer.export_network(arch, image, classes)
     params = trainer.init_params(desc, seed=seed)
@@ -67,8 +72,16 @@ def profile_compute(arch, image, classes, network_json, ks, steps=2, seed=0):
             tr = ex.trace().strip().splitlines()[1:]
             t = {int(r.split(",")[0]): float(r.split(",")[2]) - float(r.split(",")[1]) for r in tr}
             times = t if times is None else {j: min(times[j], t[j]) for j in t}
+        scale = 1.0
+        if scale_to_graph:
+            # the captured step (lr = 0: parameters unchanged), min over steps
+            ex.set_graph(True)
+            graph_ms = min(ex.step(x, y, lr=0.0)["iter_ms"] for _ in range(graph_steps + 1))
+            total = sum(times.values())
+            if total > 0 and graph_ms > 0:
+                scale = graph_ms / total
         for j, key, fl in phases:
-            rows.append(f"{k},{j},{key},{_scale_flops(fl, k, k_base)},{times[j] * 1e-3:.12g}")
+            rows.append(f"{k},{j},{key},{_scale_flops(fl, k, k_base)},{times[j] * scale * 1e-3:.12g}")
         ex.close()
     return "\n".join(rows) + "\n"
 
