@@ -50,8 +50,7 @@ int accudnn_set_conv_impl(int impl);
 int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes);
 /* split-K workspace for convolutions launched on one particular stream (a
  * concurrent weight-gradient stream) and a cap on their persistent grids
- * (max_ctas SMs, 0 = all); ptr == NULL and max_ctas == 0 removes the entry
- * (at most 4 streams) */
+ * (max_ctas SMs, 0 = all); ptr == NULL and max_ctas == 0 removes the entry */
 int accudnn_conv_set_stream_workspace(void* stream, void* ptr, unsigned long long bytes,
                                       int max_ctas);
 /* programmatic dependent launch for every kernel (default 0): the next

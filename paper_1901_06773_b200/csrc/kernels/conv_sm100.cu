@@ -39,9 +39,11 @@
 #include <array>
 #include <cstdint>
 #include <cstdlib>
+#include <memory>
 #include <sstream>
 #include <string>
 #include <unordered_map>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 
@@ -960,7 +962,9 @@ struct StreamWs {
   Workspace w;
   int max_ctas = 0;  // persistent grids on this stream use at most this many SMs (0: all)
 };
-StreamWs g_stream_ws[4];
+// one entry per registered stream (executors register their weight-gradient
+// stream); entries are heap nodes so g_cur stays valid while others come and go
+std::vector<std::unique_ptr<StreamWs>> g_stream_ws;
 Workspace* g_cur = &g_ws;
 int g_cur_ctas = 0;
 int cta_slots() { return g_cur_ctas > 0 ? std::min(g_cur_ctas, sm_count()) : sm_count(); }
@@ -1535,10 +1539,10 @@ int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, 
 void conv_select_workspace(cudaStream_t st) {
   g_cur = &g_ws;
   g_cur_ctas = 0;
-  for (StreamWs& e : g_stream_ws)
-    if (e.st && e.st == st) {
-      if (e.w.ws) g_cur = &e.w;
-      g_cur_ctas = e.max_ctas;
+  for (const auto& e : g_stream_ws)
+    if (e->st == st) {
+      if (e->w.ws) g_cur = &e->w;
+      g_cur_ctas = e->max_ctas;
     }
 }
 
@@ -1587,21 +1591,20 @@ extern "C" int accudnn_conv_set_stream_workspace(void* stream, void* ptr,
   using namespace accudnn;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!st) return static_cast<int>(cudaErrorInvalidValue);
-  for (StreamWs& e : g_stream_ws)
-    if (e.st == st) {
-      e = StreamWs{};
+  for (size_t i = 0; i < g_stream_ws.size(); ++i)
+    if (g_stream_ws[i]->st == st) {
+      if (g_cur == &g_stream_ws[i]->w) g_cur = &g_ws;
+      g_stream_ws.erase(g_stream_ws.begin() + static_cast<long>(i));
       break;
     }
   if (!ptr && max_ctas <= 0) return 0;
-  for (StreamWs& e : g_stream_ws)
-    if (!e.st) {
-      e.st = st;
-      e.w.ws = static_cast<float*>(ptr);
-      e.w.bytes = ptr ? static_cast<size_t>(bytes) : 0;
-      e.max_ctas = std::max(0, max_ctas);
-      return 0;
-    }
-  return static_cast<int>(cudaErrorMemoryAllocation);
+  auto e = std::make_unique<StreamWs>();
+  e->st = st;
+  e->w.ws = static_cast<float*>(ptr);
+  e->w.bytes = ptr ? static_cast<size_t>(bytes) : 0;
+  e->max_ctas = std::max(0, max_ctas);
+  g_stream_ws.push_back(std::move(e));
+  return 0;
 }
 
 // debug: subsequent TMA-conv launches record clock64 stamps into buf

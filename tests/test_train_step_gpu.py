@@ -375,3 +375,25 @@ def test_programmatic_dependent_launch_matches(cuda_dev):
             lib.accudnn_set_pdl(prev)
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_many_live_executors(cuda_dev):
+    """every executor registers its weight-gradient stream's split-K workspace;
+    more than a handful alive at once (and destroyed in any order) must work."""
+    arch, image, classes, k = "resnet20", 32, 12, 4
+    _, desc = trainer.export_network(arch, image, classes)
+    params = trainer.init_params(desc, seed=16)
+    x, y = data(k, image, classes, seed=110)
+    exs = [trainer.Executor(arch, image, classes, k=k) for _ in range(7)]
+    losses = []
+    for e in exs:
+        e.set_params(params)
+        e.step(x, y, lr=0.05)
+        losses.append(e.step(x, y, lr=0.05)["loss"])  # second step: side stream on
+    assert len(set(losses)) == 1
+    for i in (3, 0, 6):
+        exs[i].close()
+    e = trainer.Executor(arch, image, classes, k=k)
+    e.set_params(params)
+    e.step(x, y, lr=0.05)
+    assert e.step(x, y, lr=0.05)["loss"] == losses[0]
