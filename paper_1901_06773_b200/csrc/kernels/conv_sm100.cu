@@ -713,29 +713,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           const int col = n0 + c0 + gg * 4;
           const bool col_ok = c0 + gg * 4 < ncols;
+          // the 8 rows' destinations (and, accumulating, their old values)
+          // first: the loads are independent and all in flight at once (a
+          // load -> add -> store chain per row would pay one memory latency
+          // per row, ~30 us per 128 x 128 tile)
+          float4* d4s[8];
+          float4 olds[8];
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int m = m0 + it * 4 + rr_lo;
+            d4s[it] = nullptr;
+            if (col_ok && m < a.M)
+              d4s[it] = reinterpret_cast<float4*>(
+                  partial ? a.ws + (static_cast<long long>(split) * a.M + m) * a.Ng + col
+                          : a.out + out_row(a, m) + col);
+            olds[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (d4s[it] && a.beta && !partial) olds[it] = __ldcg(d4s[it]);
+          }
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
             const int rr = it * 4 + rr_lo;
-            const int m = m0 + rr;
             float4 o;
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                          : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w)
                          : "r"(sbuf + rr * 128 + ((gg ^ (rr & 7)) << 4)));
-            if (col_ok && m < a.M) {
-              float* dst = partial ? a.ws + (static_cast<long long>(split) * a.M + m) * a.Ng + col
-                                   : a.out + out_row(a, m) + col;
-              float4* d4 = reinterpret_cast<float4*>(dst);
+            if (d4s[it]) {
               if (a.beta && !partial) {
-                const float4 old = *d4;
-                o.x += old.x;
-                o.y += old.y;
-                o.z += old.z;
-                o.w += old.w;
+                o.x += olds[it].x;
+                o.y += olds[it].y;
+                o.z += olds[it].z;
+                o.w += olds[it].w;
               }
-              if (partial)
-                __stcg(d4, o);
-              else
-                *d4 = o;
+              __stcg(d4s[it], o);
             }
           }
         }
@@ -775,6 +784,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_dealloc<kTmemCols>(tmem);
   }
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 770] = gtimer();
+}
+
+// Strided dgrad: zero the input-gradient pixels of the parity classes that
+// receive no filter tap (row parity bit in row_empty, column parity in
+// col_empty); the classes with taps are written by their GEMMs
+__global__ void __launch_bounds__(256) dgrad_zero_empty_kernel(float4* __restrict__ dx, int n,
+                                                              int h, int w, int c4, int s,
+                                                              unsigned row_empty,
+                                                              unsigned col_empty) {
+  pdl_wait();
+  pdl_trigger();
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int row4 = w * c4;
+  for (long long row = blockIdx.x; row < static_cast<long long>(n) * h; row += gridDim.x) {
+    const int y = static_cast<int>(row % h);
+    float4* p = dx + row * row4;
+    if ((row_empty >> (y % s)) & 1u) {  // the whole image row
+      for (int i = threadIdx.x; i < row4; i += 256) __stcs(p + i, z);
+    } else {  // the pixels of the empty column classes
+      for (int i = threadIdx.x; i < row4; i += 256)
+        if ((col_empty >> ((i / c4) % s)) & 1u) __stcs(p + i, z);
+    }
+  }
 }
 
 // Deterministic split-K reduction: out[map(m)][n] (+)= sum_{s=0..S-1} ws[s][m][n],
@@ -1463,14 +1495,23 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
   *rc = 0;
   bool launched = false;
   if (any_empty && !beta) {
-    const cudaError_t e = cudaMemsetAsync(
-        dx, 0, sizeof(float) * static_cast<size_t>(d->n) * d->h * d->w * d->c, st);
+    // zero only the pixels no class GEMM writes (the others are written, not
+    // accumulated, by their class)
+    unsigned row_empty = 0, col_empty = 0;
+    for (int c = 0; c < s; ++c) {
+      if (rows[c].taps == 0) row_empty |= 1u << c;
+      if (cols[c].taps == 0) col_empty |= 1u << c;
+    }
+    const int grid = static_cast<int>(std::min<long long>(static_cast<long long>(d->n) * d->h,
+                                                          16LL * sm_count()));
+    launch_pdl(dgrad_zero_empty_kernel, grid, 256, 0, st, reinterpret_cast<float4*>(dx), d->n, d->h,
+               d->w, d->c / 4, s, row_empty, col_empty);
+    const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       *rc = static_cast<int>(e);
       return 1;
     }
     launched = true;
-    beta = 1;
   }
   for (int ca = 0; ca < s; ++ca) {
     for (int cb = 0; cb < s; ++cb) {
