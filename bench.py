@@ -218,8 +218,27 @@ def conv_kernel_us(step_fn):
             out = step_fn()
             torch.cuda.synchronize()
     keys = ("conv_sm100_kernel", "conv_igemm_kernel", "conv_splitk_reduce")
-    evs = [e for e in prof.events() if e.device_type.name == "CUDA" and any(q in e.name for q in keys)]
+    cuda = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    evs = [e for e in cuda if any(q in e.name for q in keys)]
+    bn = [e for e in cuda if "bn_fused_kernel" in e.name]
+    conv_kernel_us.bn_us = sum(e.time_range.end - e.time_range.start for e in bn)
+    conv_kernel_us.bn_launches = len(bn)
     return out, sum(e.time_range.end - e.time_range.start for e in evs), len(evs)
+
+
+def bn_min_bytes_per_step(desc, k):
+    """algorithmic (single-touch) HBM bytes of the step's batch-norm passes:
+    forward reads x (+ the shortcut) and writes y; backward reads x, dy (+ the
+    shortcut for the ReLU mask) and writes dx (+ d(shortcut))."""
+    total = 0
+    for op in desc["ops"]:
+        if op["kind"] not in ("bn", "bn_relu", "bn_add_relu"):
+            continue
+        h, w, c = op["out"]
+        S = 4 * k * h * w * c
+        tail = op["kind"] == "bn_add_relu"
+        total += (3 if tail else 2) * S + (5 if tail else 3) * S
+    return total
 
 
 # ---------------------------------------------------------------------------
@@ -432,6 +451,21 @@ def run_ours(args):
         roof["achieved"] = round(ach, 2)
         roof["frac"] = round(ach / tf32_peak, 4)
         roof["conv_kernel_ms_per_step"] = round(conv_us / 1e3, 3)
+    # the second-largest kernel family, HBM-bound: batch norm (single-touch
+    # algorithmic bytes / CUPTI device time of its kernels, same profiled step)
+    hbm_peak = float(peaks.get("hbm_gbs", 0.0)) or 6650.0  # fallback: B200_PROFILING.md
+    bn_us = getattr(conv_kernel_us, "bn_us", 0.0)
+    roofline_bn = None
+    if bn_us > 0:
+        ach_bn = bn_min_bytes_per_step(desc, k) / (bn_us * 1e-6) / 1e9
+        roofline_bn = {"bound": "hbm", "kernel": "bn_fused_kernel (cooperative / cluster single-kernel BN)",
+                       "achieved": round(ach_bn, 1), "peak": hbm_peak, "unit": "GB/s",
+                       "frac": round(ach_bn / hbm_peak, 4) if hbm_peak else None,
+                       "launches_per_step": conv_kernel_us.bn_launches,
+                       "kernel_ms_per_step": round(bn_us / 1e3, 3),
+                       "note": "algorithmic bytes = one read of every input and one write of every "
+                               "output per pass (the two-pass kernels re-read x, partly from L2); "
+                               "peak = MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
         roof["conv_kernel_launches_per_step"] = conv_launches
         roof["flops_per_launch_note"] = (
             "achieved = conv/fc fwd+dgrad+wgrad FLOPs per step / summed CUPTI device duration of "
@@ -491,6 +525,7 @@ def run_ours(args):
         "gpu_launches_note": f"kernels of one captured step counted from CUPTI records "
                              f"({all_device_ops} device activities incl. copies)",
         "roofline": roof,
+        "roofline_bn": roofline_bn,
         "roofline_official": {"img_per_s_roof": round(img_roof * world, 2),
                               "frac": round(value / (img_roof * world), 4),
                               "definition": "k / max(k*F_conv/P_tf32, B_swap/BW_host) per GPU"},
