@@ -1582,7 +1582,9 @@ void conv_select_workspace(cudaStream_t st) {
   g_cur_ctas = 0;
   for (const auto& e : g_stream_ws)
     if (e->st == st) {
-      if (e->w.ws) g_cur = &e->w;
+      // a registered stream always uses its own workspace (none: no split-K),
+      // never another stream's
+      g_cur = &e->w;
       g_cur_ctas = e->max_ctas;
     }
 }
@@ -1623,10 +1625,12 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
   return 0;
 }
 
-// a split-K workspace used only by convolutions launched on `stream` (e.g.
-// weight gradients on a side stream running concurrently with the compute
-// stream) and a cap on their persistent grids (max_ctas SMs, 0 = all);
-// ptr == NULL and max_ctas == 0 removes the stream's entry
+// a split-K workspace used only by convolutions launched on `stream` (an
+// executor's compute stream, or its weight-gradient stream running
+// concurrently with it) and a cap on their persistent grids (max_ctas SMs,
+// 0 = all).  ptr == NULL, bytes == 0 and max_ctas == 0 removes the stream's
+// entry; ptr == NULL with max_ctas < 0 registers the stream without a
+// workspace (its convolutions never split K).
 extern "C" int accudnn_conv_set_stream_workspace(void* stream, void* ptr,
                                                  unsigned long long bytes, int max_ctas) {
   using namespace accudnn;
@@ -1638,7 +1642,7 @@ extern "C" int accudnn_conv_set_stream_workspace(void* stream, void* ptr,
       g_stream_ws.erase(g_stream_ws.begin() + static_cast<long>(i));
       break;
     }
-  if (!ptr && max_ctas <= 0) return 0;
+  if (!ptr && bytes == 0 && max_ctas == 0) return 0;
   auto e = std::make_unique<StreamWs>();
   e->st = st;
   e->w.ws = static_cast<float*>(ptr);

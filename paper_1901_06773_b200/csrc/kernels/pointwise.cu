@@ -193,6 +193,18 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
   float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0};
   float fsc[4] = {0, 0, 0, 0}, fsh[4] = {0, 0, 0, 0};  // forward scale / shift
+  // forward statistics are accumulated around a per-channel pilot (the
+  // channel's value in row 0, the same for every block): sums of (x - pilot)
+  // and (x - pilot)^2 keep E[x^2] - E[x]^2 free of cancellation when
+  // |mean| >> std (shifted-data variance)
+  float pil[4] = {0, 0, 0, 0};
+  if (MODE == 0 && c_ok && !a.stats_in) {
+    const float4 p4 = __ldg(reinterpret_cast<const float4*>(a.x + c));
+    pil[0] = p4.x;
+    pil[1] = p4.y;
+    pil[2] = p4.z;
+    pil[3] = p4.w;
+  }
   if (MODE == 1 && c_ok) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -210,8 +222,9 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     if (MODE == 0) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        a0[j] += xv[j];
-        a1[j] += xv[j] * xv[j];
+        const float dx = xv[j] - pil[j];
+        a0[j] += dx;
+        a1[j] += dx * dx;
       }
     } else {
       const float dv[4] = {d.x, d.y, d.z, d.w};
@@ -405,8 +418,10 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     const int chn = blockIdx.x * ch + t;
     if (chn < a.C) {
       if (MODE == 0) {
-        const double mean = s1 / static_cast<double>(a.M);
-        double var = s2 / static_cast<double>(a.M) - mean * mean;
+        const double pilot = a.stats_in ? 0.0 : static_cast<double>(__ldg(a.x + chn));
+        const double dm = s1 / static_cast<double>(a.M);
+        const double mean = pilot + dm;
+        double var = s2 / static_cast<double>(a.M) - dm * dm;
         if (var < 0) var = 0;
         const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(a.eps)));
         const float sc = a.gamma[chn] * inv;
@@ -990,8 +1005,11 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(
     float se = 0.f;
     for (int j = lane; j < classes; j += 32) se += expf(z[j] - mx);
     se = warp_sum(se);
+    // an out-of-range label poisons the loss (NaN) and contributes no target
+    // term to the gradient instead of reading outside the row
     const int y = labels[row];
-    if (lane == 0) my_loss += mx + logf(se) - z[y];
+    const bool valid = y >= 0 && y < classes;
+    if (lane == 0) my_loss += valid ? mx + logf(se) - z[y] : __int_as_float(0x7fc00000);
     if (dlogits) {
       const float inv = 1.f / se;
       float* d = dlogits + static_cast<long long>(row) * classes;

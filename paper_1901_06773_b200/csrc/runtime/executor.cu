@@ -218,7 +218,6 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
     }
     I.stats_ok[static_cast<size_t>(o)] = ok;
   }
-  ckl(accudnn_conv_set_workspace(I.conv_ws, I.conv_ws ? conv_ws : 0), "conv workspace");
   if (cfg.autotune) accudnn_conv_autotune(1);
   ck(cudaMemset(I.params, 0, pbytes), "memset");
   ck(cudaMemset(I.grads, 0, pbytes), "memset");
@@ -252,9 +251,15 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaStreamCreateWithFlags(&I.comm_stream, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&I.input_stream, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithPriority(&I.side, cudaStreamNonBlocking, prio_lo), "stream");
-  if (I.side_ws || cfg.side_ctas > 0)
-    ckl(accudnn_conv_set_stream_workspace(I.side, I.side_ws, side_ws, cfg.side_ctas),
-        "side workspace");
+  // every stream this executor launches convolutions on owns its split-K
+  // workspace (carved out of the fixed allocation, so inside the budget):
+  // executors never share partials, whatever else is alive in the process
+  ckl(accudnn_conv_set_stream_workspace(I.compute, I.conv_ws, I.conv_ws ? conv_ws : 0,
+                                        I.conv_ws ? 0 : -1),
+      "compute workspace");
+  ckl(accudnn_conv_set_stream_workspace(I.side, I.side_ws, I.side_ws ? side_ws : 0,
+                                        cfg.side_ctas > 0 ? cfg.side_ctas : (I.side_ws ? 0 : -1)),
+      "side workspace");
   ck(cudaEventCreateWithFlags(&I.layout_done, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&I.input_ready, cudaEventDisableTiming), "event");
   auto mk = [](std::vector<cudaEvent_t>& v, size_t cnt, bool timing) {
@@ -308,6 +313,7 @@ Executor::~Executor() {
   if (I.graph) cudaGraphExecDestroy(I.graph);
   if (I.comm) ncclCommDestroy(I.comm);
   if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0, 0);
+  if (I.compute) accudnn_conv_set_stream_workspace(I.compute, nullptr, 0, 0);
   for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
                   &I.bucket_ready, &I.fork_ev, &I.wg_done})
     for (cudaEvent_t e : *v)
@@ -326,7 +332,6 @@ Executor::~Executor() {
                   static_cast<void*>(I.loss), I.conv_ws, static_cast<void*>(I.bn_stats[0]),
                   static_cast<void*>(I.bn_stats[1]), I.side_ws})
     if (p) cudaFree(p);
-  if (I.conv_ws || cfg_.budget) accudnn_conv_set_workspace(nullptr, 64ull << 20);
 }
 
 void Executor::set_params(const float* host, long long n) {
@@ -351,7 +356,19 @@ void Executor::set_comm(const void* uid, int rank, int world) {
   Impl& I = *impl_;
   // world 1 still builds a (single-rank) communicator: the bucketed
   // all-reduce path then runs on one GPU (tests)
-  if (world < 1) return;
+  if (world < 1 || rank < 0 || rank >= world)
+    throw std::invalid_argument("set_comm: need 0 <= rank < world, world >= 1");
+  // a captured iteration baked the previous communicator (or none) into its
+  // all-reduce nodes: drop it, and the old communicator with it
+  if (I.graph) cudaGraphExecDestroy(I.graph);
+  I.graph = nullptr;
+  I.graph_lr = -1.f;
+  I.graph_update = -1;
+  if (I.comm) {
+    ck(cudaStreamSynchronize(I.comm_stream), "comm drain");
+    ckn(ncclCommDestroy(I.comm), "ncclCommDestroy");
+    I.comm = nullptr;
+  }
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
   ckn(ncclCommInitRank(&I.comm, world, id, rank), "ncclCommInitRank");
@@ -653,6 +670,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       };
       if (o >= 1 && o < n) extend(o);
       if (s == 2 * n) extend(0);
+      // bucket cuts on 16-byte boundaries (the SGD kernel is float4-wide);
+      // the padding up to the next multiple of 4 belongs to the same op
+      done = (done + 3) / 4 * 4;
       prefix_after_step[static_cast<size_t>(s)] = std::min(done, net.n_params);
     }
   }

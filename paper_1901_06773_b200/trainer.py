@@ -130,6 +130,7 @@ class Executor:
                                             enc(plan_json), int(k), int(device), int(lookahead),
                                             ctypes.byref(h)), "executor create")
         self.h = h
+        self.device = int(device)
         if k <= 0:
             k = json.loads(plan_json)["k_star"]
         self.k = k
@@ -181,19 +182,48 @@ class Executor:
         _check(self.lib.accudnn_exec_trace(self.h, ctypes.byref(p)), "trace")
         return _take(p.value)
 
+    def _check_batch(self, images, labels):
+        """The kernels read images as contiguous float32 NCHW [k,3,H,W] and
+        labels as contiguous int32 [k] in [0, classes): anything else is
+        rejected here rather than reinterpreted (torch's default int64 labels
+        would read as (low, high) int32 pairs)."""
+        shape = (self.k, 3, self.image, self.image)
+        for name, a, dt, shp in (("images", images, "float32", shape),
+                                 ("labels", labels, "int32", (self.k,))):
+            if a is None:
+                continue
+            if hasattr(a, "data_ptr"):  # torch tensor
+                ok = str(a.dtype) == "torch." + dt and a.is_contiguous()
+                if a.is_cuda and a.device.index != self.device:
+                    raise ExecutorError(f"{name} on cuda:{a.device.index}, executor on cuda:{self.device}")
+            else:
+                ok = a.dtype == np.dtype(dt) and a.flags["C_CONTIGUOUS"]
+            if not ok or tuple(a.shape) != shp:
+                raise ExecutorError(f"{name}: need contiguous {dt} {list(shp)}, got "
+                                    f"{a.dtype} {list(a.shape)}")
+        if labels is not None and not (hasattr(labels, "is_cuda") and labels.is_cuda):
+            lo, hi = int(labels.min()), int(labels.max())
+            if lo < 0 or hi >= self.classes:
+                raise ExecutorError(f"labels outside [0, {self.classes}): [{lo}, {hi}]")
+
     def step(self, images, labels, lr=0.1, update=True, profile=False):
         """images: NCHW float32 [k,3,H,W]; labels int32 [k].  numpy arrays (or
         CPU torch tensors) are copied from host memory inside the step; CUDA
-        torch tensors are used in place."""
+        torch tensors are used in place (a device label outside [0, classes)
+        makes the loss NaN)."""
         host = 1
+        if not hasattr(images, "data_ptr"):
+            images = np.asarray(images)
+            labels = np.asarray(labels)
+        self._check_batch(images, labels)
         if hasattr(images, "is_cuda") and images.is_cuda:
+            if not labels.is_cuda:
+                raise ExecutorError("images on the device need device labels")
             host = 0
             ip, lp = images.data_ptr(), labels.data_ptr()
         elif hasattr(images, "data_ptr"):
             ip, lp = images.data_ptr(), labels.data_ptr()
         else:
-            images = np.ascontiguousarray(images, dtype=np.float32)
-            labels = np.ascontiguousarray(labels, dtype=np.int32)
             ip, lp = images.ctypes.data, labels.ctypes.data
         st = StepStats()
         _check(self.lib.accudnn_exec_step(self.h, ip, lp, host, float(lr), 1 if update else 0,
@@ -206,6 +236,9 @@ class Executor:
         uses the batch prefetched by the previous call; next_images (pinned
         host tensor / array) is prefetched during this step."""
         keep = []  # converted arrays must outlive the (synchronous) call
+        self._check_batch(images, labels)
+        if next_images is not None:
+            self._check_batch(next_images, None)
 
         def ptr(a, dtype=np.float32):
             if a is None:

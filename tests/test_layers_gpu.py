@@ -85,6 +85,33 @@ def test_batchnorm_fwd_bwd(cuda_dev, M, C, relu):
     assert torch.equal(y2, y_d) and torch.equal(mean2, mean_d)
 
 
+@pytest.mark.parametrize("M,C", [(42 * 56 * 56, 64), (27 * 14 * 14, 256), (8, 12)])
+def test_batchnorm_large_channel_mean(cuda_dev, M, C):
+    """|mean| = 1000 x std: E[x^2] - E[x]^2 in fp32 partial sums would lose
+    every significant digit of the variance; the kernel's shifted sums keep
+    it within 1e-4 of PyTorch's (stable) reduction."""
+    lib = _native.cuda_lib()
+    g = torch.Generator().manual_seed(7 + C)
+    x = torch.randn(M, C, generator=g) * 0.5 + 500.0 * (1.0 + torch.rand(C, generator=g))
+    gamma, beta = torch.ones(C), torch.zeros(C)
+    rm, rv = torch.zeros(C, dtype=torch.float64), torch.ones(C, dtype=torch.float64)
+    y_ref = F.batch_norm(x.double(), rm, rv, gamma.double(), beta.double(),
+                         training=True, momentum=0.1, eps=1e-5)
+    d = cuda_dev
+    x_d = x.to(d)
+    y_d = torch.empty_like(x_d)
+    mean_d, inv_d = torch.empty(C, device=d), torch.empty(C, device=d)
+    rm_d, rv_d = torch.zeros(C, device=d), torch.ones(C, device=d)
+    ws = torch.zeros(lib.accudnn_bn_workspace_bytes(C) // 4 + 1, device=d)
+    assert lib.accudnn_bn_fwd(ptr(x_d), M, C, ptr(gamma.to(d)), ptr(beta.to(d)), 1e-5, 0, ptr(y_d),
+                              ptr(mean_d), ptr(inv_d), ptr(rm_d), ptr(rv_d), 0.1, ptr(ws), None) == 0
+    torch.cuda.synchronize()
+    var = x.double().var(0, unbiased=False)
+    assert rel(1.0 / inv_d.double() ** 2 - 1e-5, var) < 1e-4
+    assert rel(y_d, y_ref) < 1e-4
+    assert rel(rv_d, rv) < 1e-4
+
+
 @pytest.mark.parametrize("M,C", [(42 * 56 * 56, 256), (27 * 14 * 14, 1024), (27 * 7 * 7, 2048),
                                  (8 * 32 * 32, 16), (5, 8)])
 def test_bn_add_relu(cuda_dev, M, C):
