@@ -25,9 +25,14 @@ typedef struct accudnn_step_stats {
   float loss;                       /* mean softmax cross-entropy of the batch */
   double iter_ms;                   /* device time of the iteration            */
   double exposed_swap_ms;           /* compute-stream stall (profiled steps)   */
-  double allreduce_ms;
-  unsigned long long peak_bytes;    /* fixed allocations + arena               */
+  double allreduce_ms;              /* NCCL all-reduce device time, summed over
+                                       the gradient buckets (profiled steps)   */
+  unsigned long long peak_bytes;    /* fixed allocations + arena (+ NCCL)      */
   unsigned long long swapped_bytes; /* featuremap bytes offloaded per step     */
+  double exposed_allreduce_ms;      /* compute-stream wait at the all-reduce
+                                       join after the last backward phase
+                                       (profiled steps): the reference's
+                                       delta_sync_s (model_ir.hpp:108)         */
 } accudnn_step_stats;
 
 const char* accudnn_rt_last_error(void);
@@ -78,6 +83,8 @@ int accudnn_exec_trace(accudnn_exec* ex, char** csv);
 /* data parallel: 128-byte NCCL unique id from rank 0, shared by the host */
 int accudnn_nccl_unique_id(void* out128);
 int accudnn_exec_set_comm(accudnn_exec* ex, const void* uid128, int rank, int world);
+/* device bytes held by the NCCL communicator (0 before set_comm) */
+unsigned long long accudnn_exec_comm_bytes(accudnn_exec* ex);
 
 #ifdef __cplusplus
 }

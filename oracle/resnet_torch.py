@@ -125,3 +125,30 @@ class TorchResNet:
         d = g + wd * w
         nb = d if first else momentum * buf + d
         return loss.item(), g, (w - lr * nb).astype(np.float32), nb.astype(np.float32)
+
+
+def init_params(describe, seed=0):
+    """Flat parameter vector with torchvision's default initialisation
+    (Kaiming-normal fan_out convs, BN gamma=1 / beta=0, FC uniform
+    +-1/sqrt(fan_in)) drawn from numpy's default_rng(seed) in op order -- the
+    same draws as the product's trainer.init_params (tests/test_oracle_pinning
+    checks they agree), restated here so the CPU reference arm of bench.py
+    needs no product module."""
+    rng = np.random.default_rng(seed)
+    p = np.zeros(describe["n_params"], dtype=np.float32)
+    for op in describe["ops"]:
+        kind = op["kind"]
+        if kind == "conv":
+            cout, cin, r = op["cout"], op["cin"], op["r"]
+            w = rng.standard_normal((cout, r, r, cin)).astype(np.float32) * (2.0 / (cout * r * r)) ** 0.5
+            if op["in0"] == -2:
+                w[..., describe["in_channels"]:] = 0.0
+            p[op["w_off"]:op["w_off"] + w.size] = w.ravel()
+        elif kind == "fc":
+            cout, cin = op["cout"], op["cin"]
+            bound = 1.0 / cin ** 0.5
+            p[op["w_off"]:op["w_off"] + cout * cin] = rng.uniform(-bound, bound, cout * cin)
+            p[op["b_off"]:op["b_off"] + cout] = rng.uniform(-bound, bound, cout)
+        elif kind in ("bn", "bn_relu", "bn_add_relu"):
+            p[op["g_off"]:op["g_off"] + op["channels"]] = 1.0
+    return p

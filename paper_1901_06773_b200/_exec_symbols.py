@@ -12,7 +12,8 @@ _ULLP = ctypes.POINTER(ctypes.c_ulonglong)
 class StepStats(ctypes.Structure):
     _fields_ = [("loss", ctypes.c_float), ("iter_ms", ctypes.c_double),
                 ("exposed_swap_ms", ctypes.c_double), ("allreduce_ms", ctypes.c_double),
-                ("peak_bytes", ctypes.c_ulonglong), ("swapped_bytes", ctypes.c_ulonglong)]
+                ("peak_bytes", ctypes.c_ulonglong), ("swapped_bytes", ctypes.c_ulonglong),
+                ("exposed_allreduce_ms", ctypes.c_double)]
 
 
 SYMBOLS = {
@@ -36,6 +37,7 @@ SYMBOLS = {
     "accudnn_exec_trace": ([_P, ctypes.POINTER(_P)], _I),
     "accudnn_nccl_unique_id": ([_P], _I),
     "accudnn_exec_set_comm": ([_P, _P, _I, _I], _I),
+    "accudnn_exec_comm_bytes": ([_P], ctypes.c_ulonglong),
 }
 
 

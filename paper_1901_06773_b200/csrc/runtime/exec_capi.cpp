@@ -190,6 +190,7 @@ int accudnn_exec_step(accudnn_exec* ex, const float* images, const int* labels, 
       out->allreduce_ms = s.allreduce_ms;
       out->peak_bytes = s.peak_bytes;
       out->swapped_bytes = s.swapped_bytes;
+      out->exposed_allreduce_ms = s.exposed_allreduce_ms;
     }
     return 0;
   });
@@ -207,6 +208,7 @@ int accudnn_exec_step_pipelined(accudnn_exec* ex, const float* images, const int
       out->allreduce_ms = s.allreduce_ms;
       out->peak_bytes = s.peak_bytes;
       out->swapped_bytes = s.swapped_bytes;
+      out->exposed_allreduce_ms = s.exposed_allreduce_ms;
     }
     return 0;
   });
@@ -240,5 +242,7 @@ int accudnn_exec_set_comm(accudnn_exec* ex, const void* uid128, int rank, int wo
     return 0;
   });
 }
+
+unsigned long long accudnn_exec_comm_bytes(accudnn_exec* ex) { return ex ? ex->ex->comm_bytes() : 0; }
 
 }  // extern "C"

@@ -72,6 +72,10 @@ struct Executor::Impl {
   std::vector<cudaEvent_t> phase_begin, phase_end;  // profiling
   cudaEvent_t iter_begin = nullptr, iter_end = nullptr, comm_done = nullptr;
   std::vector<cudaEvent_t> bucket_ready;
+  // profiled steps: all-reduce device time per bucket and the compute
+  // stream's wait at the join
+  std::vector<cudaEvent_t> ar_begin, ar_end;
+  cudaEvent_t bwd_done = nullptr, comm_joined = nullptr;
   // per-instance region predecessors: (instance index)
   std::vector<std::vector<int>> preds;
   // per-step actions
@@ -306,6 +310,10 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaEventCreate(&I.iter_begin), "event");
   ck(cudaEventCreate(&I.iter_end), "event");
   ck(cudaEventCreateWithFlags(&I.comm_done, cudaEventDisableTiming), "event");
+  mk(I.ar_begin, static_cast<size_t>(n + 2), true);
+  mk(I.ar_end, static_cast<size_t>(n + 2), true);
+  ck(cudaEventCreate(&I.bwd_done), "event");
+  ck(cudaEventCreate(&I.comm_joined), "event");
 }
 
 Executor::~Executor() {
@@ -315,10 +323,11 @@ Executor::~Executor() {
   if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0, 0);
   if (I.compute) accudnn_conv_set_stream_workspace(I.compute, nullptr, 0, 0);
   for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
-                  &I.bucket_ready, &I.fork_ev, &I.wg_done})
+                  &I.bucket_ready, &I.fork_ev, &I.wg_done, &I.ar_begin, &I.ar_end})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done, I.layout_done, I.input_ready})
+  for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done, I.layout_done, I.input_ready,
+                        I.bwd_done, I.comm_joined})
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {I.compute, I.d2h, I.h2d, I.comm_stream, I.input_stream, I.side})
     if (s) cudaStreamDestroy(s);
@@ -371,7 +380,20 @@ void Executor::set_comm(const void* uid, int rank, int world) {
   }
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
+  // NCCL's device buffers count against the cap like every other allocation
+  // (SURVEY 8e): measured as the free-memory delta around the init
+  size_t free0 = 0, free1 = 0, total = 0;
+  ck(cudaMemGetInfo(&free0, &total), "meminfo");
   ckn(ncclCommInitRank(&I.comm, world, id, rank), "ncclCommInitRank");
+  ck(cudaDeviceSynchronize(), "comm init");
+  ck(cudaMemGetInfo(&free1, &total), "meminfo");
+  comm_bytes_ = free0 > free1 ? static_cast<unsigned long long>(free0 - free1) : 0ull;
+  if (cfg_.budget && fixed_bytes_ + arena_bytes_ + comm_bytes_ > cfg_.budget)
+    std::fprintf(stderr,
+                 "[accudnn] warning: NCCL communicator holds %llu B; fixed %llu + arena %llu + "
+                 "NCCL exceed the device budget %llu B (raise m_others_bytes by the NCCL "
+                 "allowance before planning)\n",
+                 comm_bytes_, fixed_bytes_, arena_bytes_, cfg_.budget);
   I.rank = rank;
   I.world = world;
 }
@@ -678,6 +700,7 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   }
 
   const bool overlap_update = update && cfg_.overlap_update;
+  int n_buckets = 0;  // timed all-reduce buckets of a profiled step
   auto enqueue_iteration = [&](bool capture) {
     int launches = 0;
     if (host_inputs && !capture) {
@@ -771,11 +794,15 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
           ck(cudaStreamWaitEvent(I.comm_stream, I.step_done[static_cast<size_t>(s)], 0), "wait");
           if (last_wg > 0)
             ck(cudaStreamWaitEvent(I.comm_stream, I.wg_done[static_cast<size_t>(last_wg)], 0), "wait");
-          if (I.comm)
+          if (I.comm) {
+            const bool timed = profile && !capture && n_buckets < static_cast<int>(I.ar_begin.size());
+            if (timed) ck(cudaEventRecord(I.ar_begin[static_cast<size_t>(n_buckets)], I.comm_stream), "rec");
             ckn(ncclAllReduce(I.grads + reduced, I.grads + reduced,
                               static_cast<size_t>(ready - reduced), ncclFloat, ncclSum, I.comm,
                               I.comm_stream),
                 "ncclAllReduce");
+            if (timed) ck(cudaEventRecord(I.ar_end[static_cast<size_t>(n_buckets++)], I.comm_stream), "rec");
+          }
           if (overlap_update) {
             ckl(accudnn_sgd_update(I.params + reduced, I.grads + reduced, I.momentum_buf + reduced,
                                    ready - reduced, lr, cfg_.momentum, cfg_.weight_decay,
@@ -790,8 +817,11 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       }
     }
     if (comm_used) {
+      const bool timed = profile && !capture && I.comm;
+      if (timed) ck(cudaEventRecord(I.bwd_done, cs), "rec");
       ck(cudaEventRecord(I.comm_done, I.comm_stream), "record");
       ck(cudaStreamWaitEvent(cs, I.comm_done, 0), "wait");
+      if (timed) ck(cudaEventRecord(I.comm_joined, cs), "rec");
     }
     // the weight-gradient and copy streams rejoin the compute stream (graph
     // capture needs it; the update reads every gradient)
@@ -871,7 +901,7 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   ck(cudaEventElapsedTime(&ms, I.iter_begin, I.iter_end), "elapsed");
   st.loss = *I.loss_host;
   st.iter_ms = ms;
-  st.peak_bytes = fixed_bytes_ + arena_bytes_;
+  st.peak_bytes = fixed_bytes_ + arena_bytes_ + comm_bytes_;
   for (int t = 0; t < n; ++t)
     if (I.swapped[static_cast<size_t>(t)])
       st.swapped_bytes += static_cast<unsigned long long>(
@@ -896,6 +926,18 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     }
     st.exposed_swap_ms = exposed;
     trace_ = tr;
+    if (I.comm && n_buckets > 0) {
+      double ar = 0;
+      for (int b = 0; b < n_buckets; ++b) {
+        float t = 0;
+        ck(cudaEventElapsedTime(&t, I.ar_begin[static_cast<size_t>(b)], I.ar_end[static_cast<size_t>(b)]), "t");
+        ar += t;
+      }
+      float w = 0;
+      ck(cudaEventElapsedTime(&w, I.bwd_done, I.comm_joined), "t");
+      st.allreduce_ms = ar;
+      st.exposed_allreduce_ms = std::max(0.f, w);
+    }
   }
   return st;
 }

@@ -73,9 +73,10 @@ struct StepStats {
   float loss = 0.f;
   double iter_ms = 0;          // device time of the whole iteration
   double exposed_swap_ms = 0;  // compute-stream stall on prefetches (profiled steps)
-  double allreduce_ms = 0;
-  unsigned long long peak_bytes = 0;  // fixed + arena (static plan)
+  double allreduce_ms = 0;          // NCCL device time over the buckets (profiled steps)
+  unsigned long long peak_bytes = 0;  // fixed + arena (static plan) + NCCL's device bytes
   unsigned long long swapped_bytes = 0;
+  double exposed_allreduce_ms = 0;  // compute-stream wait at the all-reduce join (profiled)
 };
 
 class Executor {
@@ -102,6 +103,9 @@ class Executor {
   std::string trace_csv() const { return trace_; }
   unsigned long long arena_bytes() const { return arena_bytes_; }
   unsigned long long fixed_bytes() const { return fixed_bytes_; }
+  // device bytes NCCL allocated for the communicator (cudaMemGetInfo delta
+  // around ncclCommInitRank); charged against the budget with the rest
+  unsigned long long comm_bytes() const { return comm_bytes_; }
   int graph_launches() const { return kernel_launches_; }
 
  private:
@@ -110,7 +114,7 @@ class Executor {
   Net net_;
   ExecConfig cfg_;
   std::string trace_;
-  unsigned long long arena_bytes_ = 0, fixed_bytes_ = 0;
+  unsigned long long arena_bytes_ = 0, fixed_bytes_ = 0, comm_bytes_ = 0;
   int kernel_launches_ = 0;
 };
 

@@ -88,6 +88,32 @@ def default_m_others(describe, image, budget_bytes=None):
     return momentum + stats + staging
 
 
+def config_documents(arch, image, classes, cap_bytes, k_base=8):
+    """The planner's input documents for one BASELINE configuration, exactly
+    as bench.py and the headline plan goldens build them: network.json from
+    the exporter, hardware.json (cap, fixed overhead, measured host-link
+    bandwidth from profiles/b200/host_link.json) and model.json fitted
+    (eta = 0.95) from the committed B200 profile CSVs.  Returns
+    (network_json, hardware_json, model_json, describe)."""
+    import os
+
+    from . import planner
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pdir = os.path.join(root, "profiles", "b200")
+    network_json, desc = export_network(arch, image, classes, k_base=k_base)
+    link = {}
+    lp = os.path.join(pdir, "host_link.json")
+    if os.path.exists(lp):
+        link = json.load(open(lp))
+    pcie = float(link.get("d2h", 50.0)) * 1e9
+    m_others = default_m_others(desc, image, int(cap_bytes))
+    hw = hardware_json(int(cap_bytes), m_others, pcie)
+    csvs = [open(os.path.join(pdir, f"{arch}_{kind}_profile.csv")).read()
+            for kind in ("compute", "transfer")]
+    model_json = planner.fit(network_json, csvs, hw, eta=0.95)
+    return network_json, hw, model_json, desc
+
+
 def init_params(describe, seed=0):
     """torchvision-style initialisation of the flat parameter vector:
     Kaiming-normal (fan_out, ReLU) convs, BN gamma=1 / beta=0, FC uniform
@@ -229,7 +255,8 @@ class Executor:
         _check(self.lib.accudnn_exec_step(self.h, ip, lp, host, float(lr), 1 if update else 0,
                                           1 if profile else 0, ctypes.byref(st)), "step")
         return {"loss": st.loss, "iter_ms": st.iter_ms, "exposed_swap_ms": st.exposed_swap_ms,
-                "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes}
+                "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes,
+                "allreduce_ms": st.allreduce_ms, "exposed_allreduce_ms": st.exposed_allreduce_ms}
 
     def step_pipelined(self, images, labels, lr=0.1, update=True, next_images=None):
         """host-input step with the next batch's H2D overlapped: images=None
@@ -253,11 +280,16 @@ class Executor:
                                                     1 if update else 0, ptr(next_images),
                                                     ctypes.byref(st)), "step")
         return {"loss": st.loss, "iter_ms": st.iter_ms, "exposed_swap_ms": st.exposed_swap_ms,
-                "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes}
+                "peak_bytes": st.peak_bytes, "swapped_bytes": st.swapped_bytes,
+                "allreduce_ms": st.allreduce_ms, "exposed_allreduce_ms": st.exposed_allreduce_ms}
 
     def set_comm(self, uid_bytes, rank, world):
         buf = ctypes.create_string_buffer(bytes(uid_bytes), 128)
         _check(self.lib.accudnn_exec_set_comm(self.h, buf, int(rank), int(world)), "set_comm")
+
+    def comm_bytes(self):
+        """device bytes NCCL allocated for this executor's communicator"""
+        return self.lib.accudnn_exec_comm_bytes(self.h)
 
 
 def nccl_unique_id():

@@ -10,6 +10,9 @@ tests then pin the B200 planner against them without the reference tree.
                          FNV-1a, sweep CSV
   resnet_plans.json      exported ResNet network.json + B200 profiles ->
                          per-k evaluations and small-budget full plans
+  headline_plans.json    BASELINE configs 2-4 on bench.py's documents: the
+                         reference's full step-1 search (plan.json) and its
+                         evaluations at k* and k*+1
   resnet1001_plan.json   (--with-r1001, ~2 min) config 5: reference evaluations
                          at k* and k*+1 of ResNet-1001 under 8 GiB
 """
@@ -125,8 +128,56 @@ def resnet1001_record(R):
     return rec
 
 
+HEADLINE = [("resnet152", 224, 1000, 8 << 30),    # BASELINE config 3 (the bench line)
+            ("resnet50", 224, 1000, 12 << 30),    # config 2
+            ("resnet152", 224, 1000, 12 << 30)]   # config 4 (per GPU)
+
+
+def headline_records(R):
+    """Full Algorithm-2 searches of the reference (step = 1, planner.cpp:346-424)
+    on exactly the documents bench.py builds (trainer.config_documents), plus
+    its evaluations at k* and k*+1 (maximality)."""
+    import time
+    from paper_1901_06773_b200 import trainer
+    out = []
+    for arch, image, classes, cap in HEADLINE:
+        net, hw, model_ours, desc = trainer.config_documents(arch, image, classes, cap)
+        # the documents themselves, so the reference arm of bench.py can plan,
+        # simulate and run the CPU step without loading any product library
+        ddir = os.path.join(HERE, "headline_docs")
+        os.makedirs(ddir, exist_ok=True)
+        stem = os.path.join(ddir, f"{arch}_{image}_{cap >> 30}GiB")
+        for ext, text in (("network", net), ("hardware", hw), ("model", model_ours),
+                          ("describe", json.dumps(desc, indent=0))):
+            with open(f"{stem}.{ext}.json", "w") as f:
+                f.write(text)
+        pdir = os.path.join(ROOT, "profiles", "b200")
+        csvs = [open(os.path.join(pdir, f"{arch}_{k}_profile.csv")).read()
+                for k in ("compute", "transfer")]
+        model = planner.fit(net, csvs, hw, eta=0.95, **R)
+        t0 = time.perf_counter()
+        plan = planner.plan(net, hw, model, step=1, **R)
+        secs = time.perf_counter() - t0
+        k = json.loads(plan)["k_star"]
+        rec = {"arch": arch, "image": image, "classes": classes, "cap_bytes": cap,
+               "network_sha256": hashlib.sha256(net.encode()).hexdigest(),
+               "hardware_json": hw, "model_json": model, "plan_json": plan,
+               "k_max": planner.kmax(net, hw, **R),
+               "reference_plan_seconds_step1": round(secs, 2),
+               "evals": {str(kk): planner.evaluate_k(net, hw, model, kk, **R) for kk in (k, k + 1)}}
+        print(arch, cap >> 30, "GiB: k* =", k, "reference step-1 search %.1f s" % secs, flush=True)
+        out.append(rec)
+    return out
+
+
 def main():
     R = ref_lib()
+    if "--headline-only" in sys.argv:
+        with open(os.path.join(HERE, "headline_plans.json"), "w") as f:
+            json.dump(headline_records(R), f, indent=1)
+        return
+    with open(os.path.join(HERE, "headline_plans.json"), "w") as f:
+        json.dump(headline_records(R), f, indent=1)
     if "--with-r1001" in sys.argv:
         with open(os.path.join(HERE, "resnet1001_plan.json"), "w") as f:
             json.dump(resnet1001_record(R), f, indent=1)

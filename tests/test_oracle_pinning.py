@@ -52,10 +52,13 @@ def flat_from_torchvision(model, desc):
     return p, mapping
 
 
-def test_oracle_matches_torchvision_resnet50():
+@pytest.mark.parametrize("arch", ["resnet50", "resnet152"])
+def test_oracle_matches_torchvision_resnet(arch):
+    """the exported op graph (fused residual tails included) + flat parameter
+    layout computes torchvision's ResNet-50 / ResNet-152 exactly (fp64)"""
     torch.manual_seed(0)
-    model = tv.models.resnet50(num_classes=8).double().train()
-    _, desc = trainer.export_network("resnet50", 64, 8)
+    model = getattr(tv.models, arch)(num_classes=8).double().train()
+    _, desc = trainer.export_network(arch, 64, 8)
     params, mapping = flat_from_torchvision(model, desc)
     g = np.random.default_rng(0)
     x = g.standard_normal((2, 3, 64, 64))
@@ -96,3 +99,12 @@ def test_oracle_sgd_matches_torch_optim():
         opt.step()
         p = p_next
         assert np.allclose(p, w.detach().numpy(), rtol=1e-6, atol=1e-7)
+
+
+def test_oracle_init_equals_product_init():
+    """the CPU reference arm's parameter init (oracle) draws the same values
+    as the product's"""
+    import resnet_torch
+    for arch, image, classes in (("resnet20", 32, 12), ("resnet152", 224, 1000)):
+        _, desc = trainer.export_network(arch, image, classes)
+        assert np.array_equal(resnet_torch.init_params(desc, 3), trainer.init_params(desc, 3))
