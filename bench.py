@@ -14,10 +14,16 @@ plan (Algorithm 2 + greedy pinning -> k*, pin set), adapted learning rate
   e2e    images/s through the C ABI step with pinned HOST inputs: the H2D
          copy of the batch and the loss read-back are inside the timed step
 
-`--impl reference` times the CPU implementation of the same step (oracle
-port: plain PyTorch fp32 on all host cores, oracle/resnet_torch.py) on a
-bounded sample, plus the reference planner (oracle/_ref) on the same
-documents.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, 127.0.0.1 rendezvous); under torchrun every rank runs
+its replica and rank 0 prints the line.
+
+`--impl reference` times the reference's CPU path on the same documents
+(tests/golden/headline_docs, no product library loaded): the reference
+planner (oracle/_ref, Algorithm 2 at step 1), its simulator's modelled
+images/s for that plan, and the CPU training step (plain PyTorch fp32
+restatement, oracle/resnet_torch.py, all host cores) on a bounded sample of
+the k* batch -- its images/s is the line's value.
 """
 import argparse
 import json
@@ -45,7 +51,14 @@ def parse():
     ap.add_argument("--cap-gib", type=float, default=8.0)
     ap.add_argument("--k", type=int, default=0, help="override k* (0 = tuner)")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=2, help="images in the CPU baseline step")
+    ap.add_argument("--cpu-sample", type=int, default=4,
+                    help="images of the k* batch per CPU (reference / baseline) step")
+    ap.add_argument("--conv-math", default="tf32", choices=["tf32", "3xtf32"],
+                    help="3xtf32: fp32-accurate convolutions (split operands, 3 MMAs)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="host side only (documents, plan, rendezvous, max over ranks); no GPU")
+    ap.add_argument("--nccl-allowance-mib", type=int, default=768,
+                    help="device MiB charged to m_others for NCCL's buffers when N > 1")
     return ap.parse_args()
 
 
@@ -55,6 +68,34 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch_distributed(args):
+    """`--gpus N` (N > 1) outside torchrun: run this script under
+    torch.distributed.run with N local ranks on a free 127.0.0.1 port and
+    return its exit code (rank 0 prints the JSON line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    # NCCL's init log (ranks, channels, NVLS) on stderr, stdout stays one line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def headline_docs(arch, image, cap_gib):
+    """committed copies of the documents bench.py plans on (written by
+    tests/golden/make_golden.py from the exporter; tests pin them equal)"""
+    stem = os.path.join(ROOT, "tests", "golden", "headline_docs", f"{arch}_{image}_{int(cap_gib)}GiB")
+    if not os.path.exists(stem + ".network.json"):
+        return None
+    return {k: open(f"{stem}.{k}.json").read() for k in ("network", "hardware", "model", "describe")}
 
 
 class ClockSampler:
@@ -122,28 +163,36 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def plan_for(args, network_json, hardware_json):
-    """fit model.json from the committed B200 profiles and run the tuner."""
-    from paper_1901_06773_b200 import planner, profiler
+def plan_for(args, m_others_extra=0):
+    """documents -> k*: network.json from the exporter, model.json fitted
+    from the committed B200 profiles (trainer.config_documents, the same
+    documents the headline goldens pin), then the tuner."""
+    from paper_1901_06773_b200 import planner, profiler, trainer
+    cap = int(args.cap_gib * GIB)
     pdir = os.path.join(ROOT, "profiles", "b200")
-    cpath = os.path.join(pdir, f"{args.arch}_compute_profile.csv")
-    tpath = os.path.join(pdir, f"{args.arch}_transfer_profile.csv")
-    if os.path.exists(cpath) and os.path.exists(tpath):
-        comp, tran = open(cpath).read(), open(tpath).read()
-        source = os.path.relpath(cpath, ROOT)
+    if os.path.exists(os.path.join(pdir, f"{args.arch}_compute_profile.csv")):
+        network_json, hardware_json, model_json, desc = trainer.config_documents(
+            args.arch, args.image, args.classes, cap)
+        source = f"profiles/b200/{args.arch}_compute_profile.csv"
     else:  # profile live (first run on a new config)
+        network_json, desc = trainer.export_network(args.arch, args.image, args.classes, k_base=8)
+        link = json.load(open(os.path.join(pdir, "host_link.json")))
+        hardware_json = trainer.hardware_json(cap, trainer.default_m_others(desc, args.image, cap),
+                                              float(link.get("d2h", 50.0)) * 1e9)
         ks = profiler.grid(32)
         comp = profiler.profile_compute(args.arch, args.image, args.classes, network_json, ks)
         tran = profiler.profile_transfer(network_json, ks)
+        model_json = planner.fit(network_json, [comp, tran], hardware_json, eta=0.95)
         source = "live"
-    model_json = planner.fit(network_json, [comp, tran], hardware_json, eta=0.95)
+    if m_others_extra:
+        # data parallel: NCCL's device buffers are part of the fixed overhead
+        hw = json.loads(hardware_json)
+        hw["m_others_bytes"] += int(m_others_extra)
+        hardware_json = json.dumps(hw, indent=2) + "\n"
     t0 = time.perf_counter()
-    if args.k > 0:
-        plan_json = planner.plan(network_json, hardware_json, model_json, k_override=args.k)
-    else:
-        plan_json = planner.plan(network_json, hardware_json, model_json)
+    plan_json = planner.plan(network_json, hardware_json, model_json, k_override=max(0, args.k))
     plan_s = time.perf_counter() - t0
-    return model_json, plan_json, plan_s, source
+    return network_json, hardware_json, model_json, desc, plan_json, plan_s, source
 
 
 def conv_flops_per_image(desc):
@@ -242,73 +291,127 @@ def bn_min_bytes_per_step(desc, k):
 
 
 # ---------------------------------------------------------------------------
-def cpu_step_rate(arch, image, classes, k, threads, seed=0):
-    """oracle port: plain PyTorch fp32 training step on the host cores."""
+def _oracle_torch():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import resnet_torch
+    return resnet_torch
+
+
+def cpu_step_seconds(desc, image, classes, sample, threads, steps=1, warmup=1, seed=0):
+    """CPU training step (oracle port: plain PyTorch fp32 on the host cores,
+    oracle/resnet_torch.py) on `sample` images; returns per-step seconds."""
     import numpy as np
     import torch
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from resnet_torch import TorchResNet
-    from paper_1901_06773_b200 import trainer
+    rt = _oracle_torch()
     torch.set_num_threads(threads)
-    _, desc = trainer.export_network(arch, image, classes)
-    params = trainer.init_params(desc, seed)
+    params = rt.init_params(desc, seed)
     g = np.random.default_rng(seed)
-    x = g.standard_normal((k, 3, image, image)).astype(np.float32)
-    y = g.integers(0, classes, size=k).astype(np.int32)
-    o = TorchResNet(desc)
+    x = g.standard_normal((sample, 3, image, image)).astype(np.float32)
+    y = g.integers(0, classes, size=sample).astype(np.int32)
+    o = rt.TorchResNet(desc)
     stats = torch.zeros(desc["n_stats"])
-    o.step(params, stats, None, x, y, lr=0.1)  # warm-up
-    t0 = time.perf_counter()
-    o.step(params, stats, None, x, y, lr=0.1)
-    dt = time.perf_counter() - t0
-    return k / dt, dt
+    buf = None
+    for _ in range(warmup):
+        _, _, params, buf = o.step(params, stats, buf, x, y, lr=0.1, first=buf is None)
+    out = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, _, params, buf = o.step(params, stats, buf, x, y, lr=0.1, first=buf is None)
+        out.append(time.perf_counter() - t0)
+    return out
 
 
-def reference_planner_seconds(network_json, hardware_json, model_json):
+def reference_cpu_path(network_json, hardware_json, model_json, k_ours=None, plan_ours=None):
+    """The reference's own CPU implementation of the host path (oracle/_ref,
+    compiled from /root/reference/proj/src): Algorithm 2 at step 1 on the
+    same documents (planner.cpp:346-424), timed, and simulate_iteration of
+    its plan (simulator.cpp:79-370) -> the reference's modelled images/s.
+    With plan_ours, plan_parity says whether the documents are identical."""
     path = os.path.join(ROOT, "oracle", "_ref", "libswapsched_ref.so")
     if not os.path.exists(path):
-        return None
+        return {"unavailable": "oracle/_ref/libswapsched_ref.so not built"}
     import ctypes
     from paper_1901_06773_b200 import _native, planner
     lib = ctypes.CDLL(path)
     _native.declare_planner_symbols(lib, "oracle_")
+    R = dict(lib=lib, prefix="oracle_")
     t0 = time.perf_counter()
+    plan_ref = planner.plan(network_json, hardware_json, model_json, step=1, **R)
+    plan_s = time.perf_counter() - t0
+    k = json.loads(plan_ref)["k_star"]
+    t0 = time.perf_counter()
+    _, summ, _ = planner.simulate(network_json, hardware_json, model_json, plan_ref, "dynamic", k, **R)
+    sim_s = time.perf_counter() - t0
+    summ = json.loads(summ)
+    out = {"kind": "reference", "k_star": k, "planner_seconds_step1": round(plan_s, 3),
+           "simulate_seconds": round(sim_s, 4),
+           "modelled_iter_ms": None if summ.get("oom") else round(summ["iter_time_s"] * 1e3, 3),
+           "modelled_images_per_s": None if summ.get("oom") else round(k / summ["iter_time_s"], 2),
+           "modelled_stall_ms": None if summ.get("oom") else round(summ["total_stall_s"] * 1e3, 4)}
+    if plan_ours is not None:
+        out["plan_parity"] = plan_ref == plan_ours
+    return out
+
+
+def loaded_repo_libraries():
+    """shared objects under the repo mapped into this process"""
     try:
-        planner.plan(network_json, hardware_json, model_json, lib=lib, prefix="oracle_", step=16)
-    except planner.PlannerError:
-        pass
-    return time.perf_counter() - t0
+        maps = open("/proc/self/maps").read().splitlines()
+    except OSError:
+        return None
+    libs = {ln.split()[-1] for ln in maps if ln.endswith(".so") and ROOT in ln}
+    return sorted(os.path.relpath(p, ROOT) for p in libs)
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args):
+    """CPU reference arm: no product library on this path (documents from
+    tests/golden/headline_docs, the reference planner/simulator from
+    oracle/_ref, the CPU step from oracle/resnet_torch.py)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    docs = headline_docs(args.arch, args.image, args.cap_gib)
+    if docs is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no committed documents for {args.arch}@{args.image} "
+                          f"{args.cap_gib:g} GiB (tests/golden/make_golden.py HEADLINE)"}), flush=True)
+        return
     threads = os.cpu_count() or 1
-    from paper_1901_06773_b200 import trainer
-    k = args.k or 24
-    rates = []
-    for _ in range(max(1, args.warmup)):
-        cpu_step_rate(args.arch, args.image, args.classes, args.cpu_sample, threads)
-    for _ in range(max(1, args.steps)):
-        r, _ = cpu_step_rate(args.arch, args.image, args.classes, args.cpu_sample, threads)
-        rates.append(r)
-    value = sum(rates) / len(rates)
+    ref = reference_cpu_path(docs["network"], docs["hardware"], docs["model"])
+    k = args.k or ref.get("k_star") or 0
+    desc = json.loads(docs["describe"])
+    # bounded sample: as many of the k* images per step as keep the whole
+    # --steps/--warmup run within ~150 s on this host (at most --cpu-sample)
+    steps, warm = max(1, args.steps), max(1, args.warmup)
+    probe = cpu_step_seconds(desc, args.image, args.classes, 1, threads, steps=1, warmup=1)[0]
+    sample = int(max(1, min(args.cpu_sample, k or args.cpu_sample, 150.0 / ((steps + warm) * probe))))
+    secs = cpu_step_seconds(desc, args.image, args.classes, sample, threads, steps=steps,
+                            warmup=max(0, warm - 1))
+    ms = 1e3 * sum(secs) / len(secs)
+    value = sample / (ms * 1e-3)
     line = {
         "impl": "reference", "metric": "images/s (ResNet-152 training step, tuned minibatch, "
-        "device cap)", "value": round(value, 3), "unit": "images/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * args.cpu_sample / value, 2),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "device cap)", "value": round(value, 3), "unit": "images/s", "n_gpus": 0,
+        "launched_with_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic N(0,1) images, uniform labels, torchvision-style init",
-        "config": {"workload": f"{args.arch}@{args.image} training step, k*={k} per GPU "
-                   f"(bounded sample of {args.cpu_sample} images per timed step)",
-                   "cap_gib": args.cap_gib},
+        "config": {"workload": f"{args.arch}@{args.image}, {args.cap_gib:g} GiB device cap per GPU, "
+                   f"tuner k*={k} per GPU, global batch {k}",
+                   "model": args.arch, "k_star": k, "cap_bytes": int(args.cap_gib * GIB),
+                   "same_config": True,
+                   "sample": f"{sample} of the k*={k} images per timed step (a bounded sample; "
+                             "images/s = sample / step time)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads,
-                         "kind": "port", "sample": f"{args.cpu_sample} images/step, torch fp32 "
-                         "CPU restatement (oracle/resnet_torch.py)"},
+                         "kind": "port",
+                         "sample": f"{sample} images per step, {steps} steps: the training "
+                                   "step restated in plain PyTorch fp32 (oracle/resnet_torch.py; the "
+                                   "reference has no layer math)"},
+        "reference_planner": ref,
         "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_libraries_loaded": loaded_repo_libraries(),
     }
     print(json.dumps(line), flush=True)
 
@@ -320,23 +423,22 @@ def run_ours(args):
     from paper_1901_06773_b200 import planner, trainer
 
     world, rank, local = dist_env()
+    if args.dry_run:
+        return run_dry(args, world, rank)
     if "ACCUDNN_PDL" in os.environ:  # A/B switch for programmatic dependent launch
         trainer._lib().accudnn_set_pdl(int(os.environ["ACCUDNN_PDL"]))
+    if args.conv_math == "3xtf32":
+        trainer._lib().accudnn_set_conv_math(1)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
     # ---- host side of the path: spec, profiles -> model, tuner -> plan, LR ----
-    network_json, desc = trainer.export_network(args.arch, args.image, args.classes, k_base=8)
-    link = {}
-    lp = os.path.join(ROOT, "profiles", "b200", "host_link.json")
-    if os.path.exists(lp):
-        link = json.load(open(lp))
-    pcie = float(link.get("d2h", 50.0)) * 1e9
-    m_others = trainer.default_m_others(desc, args.image, int(args.cap_gib * GIB))
-    hardware_json = trainer.hardware_json(int(args.cap_gib * GIB), m_others, pcie)
-    model_json, plan_json, plan_s, prof_src = plan_for(args, network_json, hardware_json)
+    # (every rank plans on identical documents: identical k* and pins; N > 1
+    # charges NCCL's device buffers to the fixed overhead before planning)
+    extra = (args.nccl_allowance_mib << 20) if world > 1 else 0
+    network_json, hardware_json, model_json, desc, plan_json, plan_s, prof_src = plan_for(args, extra)
     plan = json.loads(plan_json)
     k = plan["k_star"]
     q = world * k / 8.0
@@ -348,6 +450,8 @@ def run_ours(args):
     tune_path = os.path.join(ROOT, "profiles", "b200", "conv_tune.txt")
     if os.path.exists(tune_path) and not os.environ.get("ACCUDNN_RETUNE"):
         _native.conv_tune_import(open(tune_path).read())
+    torch.cuda.synchronize()
+    free_before_exec, _ = torch.cuda.mem_get_info(dev)
     ex = trainer.Executor(args.arch, args.image, args.classes, mode="dynamic", plan_json=plan_json,
                           network_json=network_json, hardware_json=hardware_json, device=local)
     ex.set_params(trainer.init_params(desc, seed=0))
@@ -489,34 +593,64 @@ def run_ours(args):
     t_swap = swapped / pcie if swapped else 0.0
     img_roof = k / max(t_conv, t_swap)
 
+    # data parallel: all-reduce device time and the compute stream's wait at
+    # its join, measured in the profiled step; the exposed part is the
+    # reference's per-iteration delta_sync_s (model_ir.hpp:108,
+    # perf_model.cpp:141-143), written back into hardware.json
+    dp = None
+    if world > 1:
+        ar = max_over_ranks(prof.get("exposed_allreduce_ms", 0.0))
+        hw = json.loads(hardware_json)
+        hw["delta_sync_s"] = ar * 1e-3
+        hw_delta = json.dumps(hw, indent=2) + "\n"
+        pred = json.loads(plan_json).get("predicted_iter_time_s")
+        dp = {"allreduce_ms": round(max_over_ranks(prof.get("allreduce_ms", 0.0)), 3),
+              "exposed_allreduce_ms": round(ar, 3), "delta_sync_s": ar * 1e-3,
+              "grad_bytes": 4 * desc["n_params"], "bucket_bytes": 25 << 20,
+              "nccl_device_bytes": int(max_over_ranks(float(ex.comm_bytes()))),
+              "nccl_allowance_bytes": extra,
+              "predicted_iter_ms_with_delta": None if pred is None else round((pred + ar * 1e-3) * 1e3, 3)}
+        if rank == 0:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            with open(os.path.join(ROOT, "gpurun_out", f"hardware_dp{world}.json"), "w") as f:
+                f.write(hw_delta)
+    free_after, total_mem = torch.cuda.mem_get_info(dev)
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    # ---- CPU legs (after the timed region): the reference's planner +
+    # simulator on the same documents (plan parity), and the CPU step ----
     try:
-        cpu_rate, cpu_dt = cpu_step_rate(args.arch, args.image, args.classes, args.cpu_sample,
-                                         threads)
-    except Exception as e:  # never fail the GPU line on the CPU baseline
+        ref = reference_cpu_path(network_json, hardware_json, model_json, plan_ours=plan_json)
+    except Exception as e:  # never fail the GPU line on a baseline
+        ref = {"error": str(e)}
+    try:
+        secs = cpu_step_seconds(desc, args.image, args.classes, min(k, args.cpu_sample), threads)
+        cpu_rate, cpu_dt = min(k, args.cpu_sample) / secs[0], secs[0]
+    except Exception as e:
         cpu_rate, cpu_dt = None, str(e)
-    ref_plan_s = None
-    try:
-        ref_plan_s = reference_planner_seconds(network_json, hardware_json, model_json)
-    except Exception:
-        pass
     clk = clocks.summary()
     n_fm = len(desc["ops"])
+    arch_name = {"resnet152": "ResNet-152", "resnet50": "ResNet-50", "resnet20": "ResNet-20",
+                 "resnet1001": "ResNet-1001"}.get(args.arch, args.arch)
     line = {
-        "metric": "images/s (ResNet-152 training step, tuned minibatch, device cap)",
+        "metric": f"images/s ({arch_name} training step, tuned minibatch, device cap)",
         "value": round(value, 2), "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TF32 tensor-core convolutions)",
-        "data": "synthetic N(0,1) 224x224 images, uniform labels, torchvision-style random init",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (TF32 tensor-core convolutions)" if args.conv_math == "tf32"
+                 else "f32 (3xTF32 convolutions: fp32-accurate)",
+        "data": f"synthetic N(0,1) {args.image}x{args.image} images, uniform labels, "
+                "torchvision-style random init",
         "config": {"workload": f"{args.arch}@{args.image}, {args.cap_gib:g} GiB device cap per GPU, "
                    f"tuner k*={k} per GPU, global batch {world * k}",
                    "model": args.arch, "global_batch": world * k, "k_star": k,
                    "parallelism": f"dp{world}", "cap_bytes": int(args.cap_gib * GIB),
                    "pinned_featuremaps": f"{len(plan['pinned_objects'])}/{n_fm}",
                    "lr_alpha_star": lr, "cuda_graph": not args.no_graph,
-                   "l2": "inputs > L2: each step streams ~k*273 MiB of activations",
+                   "conv_math": args.conv_math,
+                   "l2": "inputs > L2: each step streams the batch's activations "
+                         f"(~{sum(4 * o['out'][0] * o['out'][1] * o['out'][2] for o in desc['ops']) * k >> 20} MiB)",
                    "profiles": prof_src},
         "e2e": {"value": round(e2e_value, 2), "unit": "images/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 4 + y_host.numel() * 4),
@@ -529,24 +663,71 @@ def run_ours(args):
         "roofline_official": {"img_per_s_roof": round(img_roof * world, 2),
                               "frac": round(value / (img_roof * world), 4),
                               "definition": "k / max(k*F_conv/P_tf32, B_swap/BW_host) per GPU"},
-        "memory": {"peak_device_bytes": int(arena + fixed), "arena_bytes": int(arena),
-                   "fixed_bytes": int(fixed), "cap_bytes": int(args.cap_gib * GIB)},
+        "memory": {"peak_device_bytes": int(arena + fixed + ex.comm_bytes()), "arena_bytes": int(arena),
+                   "fixed_bytes": int(fixed), "nccl_bytes": int(ex.comm_bytes()),
+                   "cap_bytes": int(args.cap_gib * GIB),
+                   "measured_executor_device_bytes": int(free_before_exec - free_after),
+                   "measured_process_device_bytes": int(total_mem - free_after),
+                   "note": "measured_* = cudaMemGetInfo deltas: executor = free before its "
+                           "construction minus free after the timed steps (arena, fixed "
+                           "buffers, NCCL, CUDA-graph and library internals); process "
+                           "additionally holds the CUDA context and torch's input tensors"},
         "swap": {"swapped_bytes_per_step": int(swapped),
                  "exposed_swap_ms": round(prof["exposed_swap_ms"], 3),
                  "exposed_swap_frac": round(prof["exposed_swap_ms"] / max(prof["iter_ms"], 1e-9), 4)},
-        "planner": {"plan_seconds_b200_host": round(plan_s, 4),
-                    "reference_planner_seconds_step16": None if ref_plan_s is None else round(ref_plan_s, 3)},
+        "dp": dp,
+        "planner": {"plan_seconds_b200_host": round(plan_s, 4), "reference": ref,
+                    "plan_parity": ref.get("plan_parity")},
         "clocks": clk,
         "cpu_baseline": {"value": None if cpu_rate is None else round(cpu_rate, 3),
                          "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.cpu_sample} images, one torch fp32 CPU step "
-                                   f"({cpu_dt if isinstance(cpu_dt, str) else round(cpu_dt, 2)} s)"},
+                         "sample": f"{min(k, args.cpu_sample)} of the k* images, one torch fp32 CPU "
+                                   f"step ({cpu_dt if isinstance(cpu_dt, str) else round(cpu_dt, 2)} s; "
+                                   "oracle/resnet_torch.py -- the reference has no layer math); "
+                                   "the reference's own CPU path (planner + simulator) is "
+                                   "planner.reference"},
     }
     print(json.dumps(line), flush=True)
 
 
+def run_dry(args, world, rank):
+    """Host side of every rank without a GPU (CPU tests of the launcher):
+    documents and plan per rank, gloo rendezvous, k* / plan digest gathered
+    and checked equal across ranks, max over ranks, one line from rank 0."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    extra = (args.nccl_allowance_mib << 20) if world > 1 else 0
+    t0 = time.perf_counter()
+    network_json, hardware_json, model_json, desc, plan_json, plan_s, src = plan_for(args, extra)
+    k = json.loads(plan_json)["k_star"]
+    digest = int(hashlib.sha256(plan_json.encode()).hexdigest()[:12], 16)
+    mine = torch.tensor([float(k), float(digest), time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        allv = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allv, mine)
+        dist.barrier()
+    else:
+        allv = [mine]
+    same = all(float(v[0]) == k and float(v[1]) == digest for v in allv)
+    if rank == 0:
+        print(json.dumps({"metric": "images/s (dry run: host side only)", "value": None,
+                          "unit": "images/s", "n_gpus": world, "dry_run": True, "k_star": k,
+                          "global_batch": world * k, "plans_identical_across_ranks": same,
+                          "host_seconds_max_over_ranks": round(max(float(v[2]) for v in allv), 4),
+                          "m_others_extra_bytes": extra}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    world, _, _ = dist_env()
+    if args.gpus > 1 and world == 1 and "TORCHELASTIC_RUN_ID" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     else:

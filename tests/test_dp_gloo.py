@@ -91,3 +91,24 @@ def test_two_rank_plan_and_buckets():
         assert covered == n_params or n_params - covered < 4
         assert 0.1 < lr < 1.0
     assert res[0][5] == res[1][5]
+
+
+@pytest.mark.parametrize("gpus", [2, 3])
+def test_bench_launcher_spawns_ranks(gpus):
+    """`python bench.py --gpus N` outside torchrun re-launches itself under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous); every rank
+    plans on identical documents with NCCL's allowance charged to m_others,
+    and rank 0 alone prints one JSON line with n_gpus = N (--dry-run: host
+    side only, gloo)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run",
+                          "--gpus", str(gpus)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == gpus and rec["plans_identical_across_ranks"]
+    assert rec["m_others_extra_bytes"] == 768 << 20
+    assert rec["global_batch"] == gpus * rec["k_star"]
