@@ -80,6 +80,13 @@ int accudnn_exec_memory(accudnn_exec* ex, unsigned long long* arena_bytes,
                         unsigned long long* fixed_bytes);
 int accudnn_exec_launches(accudnn_exec* ex);
 int accudnn_exec_trace(accudnn_exec* ex, char** csv);
+/* documents of the last profiled step in the reference simulator's schemas
+ * (/root/reference/proj/src/simulator.cpp:419-473), from CUDA events on every
+ * phase and copy: which = "trace" (trace.csv), "mem_curves", "stall_bars",
+ * "summary" (summary.json); "order" = the copies of an iteration in stream
+ * order, one "swap_out fmN" / "swap_in fmN" per line.  Free with
+ * accudnn_rt_free. */
+int accudnn_exec_document(accudnn_exec* ex, const char* which, char** out);
 /* data parallel: 128-byte NCCL unique id from rank 0, shared by the host */
 int accudnn_nccl_unique_id(void* out128);
 int accudnn_exec_set_comm(accudnn_exec* ex, const void* uid128, int rank, int world);

@@ -35,6 +35,7 @@ SYMBOLS = {
     "accudnn_exec_memory": ([_P, _ULLP, _ULLP], _I),
     "accudnn_exec_launches": ([_P], _I),
     "accudnn_exec_trace": ([_P, ctypes.POINTER(_P)], _I),
+    "accudnn_exec_document": ([_P, _S, ctypes.POINTER(_P)], _I),
     "accudnn_nccl_unique_id": ([_P], _I),
     "accudnn_exec_set_comm": ([_P, _P, _I, _I], _I),
     "accudnn_exec_comm_bytes": ([_P], ctypes.c_ulonglong),

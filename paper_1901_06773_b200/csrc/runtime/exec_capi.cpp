@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -12,6 +13,7 @@
 
 #include "accudnn.h"
 #include "executor.h"
+#include "swapsched/api.hpp"
 #include "net.h"
 
 using nlohmann::json;
@@ -45,6 +47,78 @@ int guarded(F&& f) {
     g_err = e.what();
     return 3;
   }
+}
+
+// The executor's real timeline as the reference simulator's event list
+// (simulator.hpp SimEvent / SimSummary): kernel_start / kernel_end per phase
+// on the compute stream, xfer_start / xfer_end per copy on the swap streams,
+// mem_used_after = fixed + the live instance bytes of the phase the event
+// falls in; ordered by (time, stream) as simulator.cpp:56-75 orders equal
+// times.  Serialised by the same functions as the simulated documents
+// (simulator.cpp:419-473), so simulated and real timelines diff directly.
+struct RealDocs {
+  std::vector<swapsched::SimEvent> events;
+  swapsched::SimSummary summary;
+};
+
+RealDocs real_docs(const accudnn::RealTimeline& tl) {
+  using swapsched::EventKind;
+  using swapsched::Stream;
+  RealDocs d;
+  const size_t P = tl.kstart.size();
+  auto mem_at = [&](long long t) -> unsigned long long {
+    // the last phase that started at or before t
+    size_t j = static_cast<size_t>(std::upper_bound(tl.kstart.begin(), tl.kstart.end(), t) -
+                                   tl.kstart.begin());
+    if (j > 0) --j;
+    return P ? static_cast<unsigned long long>(tl.mem_at_phase[j]) : tl.fixed;
+  };
+  struct Ev {
+    long long t;
+    int stream;
+    size_t seq;
+    swapsched::SimEvent e;
+  };
+  std::vector<Ev> ev;
+  auto add = [&](long long t, Stream st, EventKind k, std::string subject) {
+    swapsched::SimEvent e;
+    e.time = t;
+    e.stream = st;
+    e.kind = k;
+    e.subject = std::move(subject);
+    e.mem_used_after = mem_at(t);
+    ev.push_back({t, static_cast<int>(st), ev.size(), std::move(e)});
+  };
+  for (size_t j = 0; j < P; ++j) {
+    add(tl.kstart[j], Stream::compute, EventKind::kernel_start, "phase " + std::to_string(j + 1));
+    add(tl.kend[j], Stream::compute, EventKind::kernel_end, "phase " + std::to_string(j + 1));
+  }
+  for (const auto& c : tl.copies) {
+    const Stream st = c.stream == 1 ? Stream::swap_out : Stream::swap_in;
+    const std::string name = "fm" + std::to_string(c.tensor + 1);
+    add(c.start, st, EventKind::xfer_start, name);
+    add(c.end, st, EventKind::xfer_end, name);
+  }
+  std::stable_sort(ev.begin(), ev.end(), [](const Ev& a, const Ev& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.stream != b.stream) return a.stream < b.stream;
+    return a.seq < b.seq;
+  });
+  for (auto& e : ev) d.events.push_back(std::move(e.e));
+  auto& s = d.summary;
+  s.kernel_start.assign(tl.kstart.begin(), tl.kstart.end());
+  s.kernel_end.assign(tl.kend.begin(), tl.kend.end());
+  s.per_phase_stall.assign(P, 0);
+  long long prev = 0;
+  for (size_t j = 0; j < P; ++j) {
+    s.per_phase_stall[j] = std::max(0LL, tl.kstart[j] - prev);
+    prev = tl.kend[j];
+    s.total_stall += s.per_phase_stall[j];
+  }
+  s.iter_time = P ? tl.kend.back() : 0;
+  s.peak_mem = tl.fixed;
+  for (long long m : tl.mem_at_phase) s.peak_mem = std::max<unsigned long long>(s.peak_mem, m);
+  return d;
 }
 
 }  // namespace
@@ -97,6 +171,9 @@ int accudnn_exec_create(const char* arch, int image, int classes, const char* mo
     if (const char* e = std::getenv("ACCUDNN_OVERLAP_UPDATE")) cfg.overlap_update = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_CONV_BN_STATS")) cfg.conv_bn_stats = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_SIDE_WS_FRAC")) cfg.side_ws_frac = std::atof(e);
+    // ACCUDNN_PREFETCH=lookahead: fixed-lookahead swap-in instead of the queue
+    if (const char* e = std::getenv("ACCUDNN_PREFETCH"))
+      cfg.prefetch_queue = std::string(e) == "lookahead" ? 0 : 1;
     const accudnn::Net net = accudnn::build_net(arch, image, classes);
     const int n = net.num_ops();
     const std::string m = mode ? mode : "resident";
@@ -225,6 +302,30 @@ int accudnn_exec_launches(accudnn_exec* ex) { return ex->ex->graph_launches(); }
 int accudnn_exec_trace(accudnn_exec* ex, char** csv) {
   return guarded([&] {
     *csv = dup_out(ex->ex->trace_csv());
+    return 0;
+  });
+}
+
+int accudnn_exec_document(accudnn_exec* ex, const char* which, char** out) {
+  return guarded([&] {
+    const std::string w = which ? which : "";
+    if (w == "order") {
+      std::string o;
+      for (const auto& line : ex->ex->copy_order()) o += line + "\n";
+      *out = dup_out(o);
+      return 0;
+    }
+    const RealDocs d = real_docs(ex->ex->timeline());
+    if (w == "trace")
+      *out = dup_out(swapsched::trace_to_csv(d.events));
+    else if (w == "mem_curves")
+      *out = dup_out(swapsched::mem_curves_csv(d.events, ex->ex->timeline().fixed));
+    else if (w == "stall_bars")
+      *out = dup_out(swapsched::stall_bars_csv(d.summary));
+    else if (w == "summary")
+      *out = dup_out(swapsched::summary_to_json(d.summary));
+    else
+      throw std::invalid_argument("unknown document '" + w + "'");
     return 0;
   });
 }

@@ -5,6 +5,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
+#include <functional>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -75,6 +77,8 @@ struct Executor::Impl {
   // profiled steps: all-reduce device time per bucket and the compute
   // stream's wait at the join
   std::vector<cudaEvent_t> ar_begin, ar_end;
+  // profiled steps: every copy's start / end (timing events per tensor)
+  std::vector<cudaEvent_t> out_b, out_e, in_b, in_e;
   cudaEvent_t bwd_done = nullptr, comm_joined = nullptr;
   // per-instance region predecessors: (instance index)
   std::vector<std::vector<int>> preds;
@@ -107,34 +111,7 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
     if (net_.ops[static_cast<size_t>(t)].transient) I.swapped[static_cast<size_t>(t)] = 0;
   ck(cudaSetDevice(cfg.device), "cudaSetDevice");
 
-  // ---- static arena plan ----
   I.lm = build_lifetimes(net_, cfg.k, I.swapped, cfg.lookahead, kAlign);
-  const long long arena = plan_arena(I.lm);
-  arena_bytes_ = static_cast<unsigned long long>(arena);
-
-  // region predecessors: earlier (in time) instances sharing bytes
-  I.preds.assign(I.lm.inst.size(), {});
-  for (size_t a = 0; a < I.lm.inst.size(); ++a) {
-    const Instance& x = I.lm.inst[a];
-    for (size_t b = 0; b < I.lm.inst.size(); ++b) {
-      const Instance& y = I.lm.inst[b];
-      if (a == b || y.last >= x.first) continue;
-      if (y.offset < x.offset + x.bytes && x.offset < y.offset + y.bytes)
-        I.preds[a].push_back(static_cast<int>(b));
-    }
-  }
-  I.prefetch_at.assign(static_cast<size_t>(2 * n + 2), {});
-  I.offload_at.assign(static_cast<size_t>(2 * n + 2), {});
-  I.first_compute_write.assign(static_cast<size_t>(2 * n + 2), {});
-  for (int t = 0; t < n; ++t) {
-    if (!I.swapped[static_cast<size_t>(t)]) continue;
-    I.offload_at[static_cast<size_t>(fwd_step(t))].push_back(t);
-    const Instance& p = I.lm.inst[static_cast<size_t>(I.lm.pre_inst[static_cast<size_t>(t)])];
-    I.prefetch_at[static_cast<size_t>(p.first)].push_back(t);
-  }
-  for (size_t i = 0; i < I.lm.inst.size(); ++i)
-    if (I.lm.inst[i].kind != InstKind::act_prefetched)
-      I.first_compute_write[static_cast<size_t>(I.lm.inst[i].first)].push_back(static_cast<int>(i));
 
   // ---- fixed allocations (the planner's fixed overhead) ----
   const long long k = cfg.k;
@@ -179,6 +156,78 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
     side_ws = static_cast<size_t>(static_cast<double>(conv_ws) * f) & ~static_cast<size_t>(4095);
     conv_ws -= side_ws;
   }
+  // ---- static arena plan ----
+  // The reference runtime model frees a swapped featuremap when its offload
+  // lands and claims pool bytes for a prefetch as soon as they are free, in
+  // GMAP order (simulator.cpp:113-140, :185-194, :233-285).  In the static
+  // arena: (1) a swapped activation's region is kept out of reuse for `pad`
+  // phases after its last forward reader (its offload drains) while the
+  // budget has room; (2) the swap-in queue issues prefetches as early as the
+  // budget leaves room (schedule_prefetches).  The largest pad whose packing
+  // fits the budget wins; if first-fit packing overshoots, the room given to
+  // the queue shrinks by the overshoot; the fixed lookahead placement with no
+  // pad is the fallback.
+  {
+    bool any_swap = false;
+    for (char c : I.swapped) any_swap = any_swap || c;
+    long long arena = plan_arena(I.lm);
+    if (cfg.prefetch_queue && any_swap && cfg.budget && fixed_bytes_ < cfg.budget) {
+      const LifetimeModel base = I.lm;
+      const long long base_arena = arena;
+      bool ok = false;
+      for (int pad : {2 * n, 16, 4, 0}) {
+        LifetimeModel padded = base;
+        for (Instance& x : padded.inst)
+          if (x.kind == InstKind::act && x.swapped) x.pack_last = std::min(2 * n, x.last + pad);
+        long long room = static_cast<long long>(cfg.budget - fixed_bytes_);
+        for (int it = 0; it < 8 && room > 0 && !ok; ++it) {
+          I.lm = padded;
+          schedule_prefetches(net_, I.lm, room);
+          arena = plan_arena(I.lm);
+          const long long over = static_cast<long long>(fixed_bytes_) + arena -
+                                 static_cast<long long>(cfg.budget);
+          if (over <= 0)
+            ok = true;
+          else
+            room -= over;
+        }
+        if (ok) break;
+      }
+      if (!ok) {
+        I.lm = base;
+        arena = base_arena;
+      }
+    }
+    arena_bytes_ = static_cast<unsigned long long>(arena);
+  }
+  const long long arena = static_cast<long long>(arena_bytes_);
+  // region predecessors: earlier (in time) instances sharing bytes
+  I.preds.assign(I.lm.inst.size(), {});
+  for (size_t a = 0; a < I.lm.inst.size(); ++a) {
+    const Instance& x = I.lm.inst[a];
+    for (size_t b = 0; b < I.lm.inst.size(); ++b) {
+      const Instance& y = I.lm.inst[b];
+      if (a == b || y.last >= x.first) continue;
+      if (y.offset < x.offset + x.bytes && x.offset < y.offset + y.bytes)
+        I.preds[a].push_back(static_cast<int>(b));
+    }
+  }
+  I.prefetch_at.assign(static_cast<size_t>(2 * n + 2), {});
+  I.offload_at.assign(static_cast<size_t>(2 * n + 2), {});
+  I.first_compute_write.assign(static_cast<size_t>(2 * n + 2), {});
+  for (int t = 0; t < n; ++t) {
+    if (!I.swapped[static_cast<size_t>(t)]) continue;
+    I.offload_at[static_cast<size_t>(fwd_step(t))].push_back(t);
+    const Instance& p = I.lm.inst[static_cast<size_t>(I.lm.pre_inst[static_cast<size_t>(t)])];
+    I.prefetch_at[static_cast<size_t>(p.first)].push_back(t);
+  }
+  // within a phase, the swap-in stream takes its prefetches in GMAP order
+  // (fm_{t+1} is prefetched in phase 2N - t: larger t first)
+  for (auto& v : I.prefetch_at) std::sort(v.begin(), v.end(), std::greater<int>());
+  for (size_t i = 0; i < I.lm.inst.size(); ++i)
+    if (I.lm.inst[i].kind != InstKind::act_prefetched)
+      I.first_compute_write[static_cast<size_t>(I.lm.inst[i].first)].push_back(static_cast<int>(i));
+
   if (cfg.budget) {
     if (cfg.fixed_allowance && fixed_bytes_ > cfg.fixed_allowance)
       throw std::runtime_error("fixed device allocations (" + std::to_string(fixed_bytes_) +
@@ -310,6 +359,10 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaEventCreate(&I.iter_begin), "event");
   ck(cudaEventCreate(&I.iter_end), "event");
   ck(cudaEventCreateWithFlags(&I.comm_done, cudaEventDisableTiming), "event");
+  mk(I.out_b, static_cast<size_t>(n), true);
+  mk(I.out_e, static_cast<size_t>(n), true);
+  mk(I.in_b, static_cast<size_t>(n), true);
+  mk(I.in_e, static_cast<size_t>(n), true);
   mk(I.ar_begin, static_cast<size_t>(n + 2), true);
   mk(I.ar_end, static_cast<size_t>(n + 2), true);
   ck(cudaEventCreate(&I.bwd_done), "event");
@@ -323,7 +376,7 @@ Executor::~Executor() {
   if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0, 0);
   if (I.compute) accudnn_conv_set_stream_workspace(I.compute, nullptr, 0, 0);
   for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
-                  &I.bucket_ready, &I.fork_ev, &I.wg_done, &I.ar_begin, &I.ar_end})
+                  &I.bucket_ready, &I.fork_ev, &I.wg_done, &I.ar_begin, &I.ar_end, &I.out_b, &I.out_e, &I.in_b, &I.in_e})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {I.iter_begin, I.iter_end, I.comm_done, I.layout_done, I.input_ready,
@@ -701,8 +754,13 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
 
   const bool overlap_update = update && cfg_.overlap_update;
   int n_buckets = 0;  // timed all-reduce buckets of a profiled step
+  std::vector<std::string> order;  // copies in enqueue (= stream) order
+  RealTimeline timeline;
   auto enqueue_iteration = [&](bool capture) {
     int launches = 0;
+    const bool timed_copies = profile && !capture;
+    order.clear();
+    timeline.copies.clear();
     if (host_inputs && !capture) {
       const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
       if (images)
@@ -737,10 +795,14 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
             ck(cudaStreamWaitEvent(I.h2d, I.d2h_done[static_cast<size_t>(y.tensor)], 0), "wait");
           ck(cudaStreamWaitEvent(I.h2d, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
         }
+        if (timed_copies) ck(cudaEventRecord(I.in_b[static_cast<size_t>(t)], I.h2d), "rec");
         ck(cudaMemcpyAsync(I.arena + p.offset, I.host_store[static_cast<size_t>(t)],
                            static_cast<size_t>(p.bytes), cudaMemcpyHostToDevice, I.h2d),
            "prefetch");
+        if (timed_copies) ck(cudaEventRecord(I.in_e[static_cast<size_t>(t)], I.h2d), "rec");
         ck(cudaEventRecord(I.h2d_done[static_cast<size_t>(t)], I.h2d), "record");
+        order.push_back("swap_in fm" + std::to_string(t + 1));
+        timeline.copies.push_back({2, t, 0, 0});
       }
       // compute: inputs that were prefetched must have landed
       const bool fwd = s <= n;
@@ -780,10 +842,14 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
       for (int t : I.offload_at[static_cast<size_t>(s)]) {
         const Instance& a = I.lm.inst[static_cast<size_t>(I.lm.act_inst[static_cast<size_t>(t)])];
         ck(cudaStreamWaitEvent(I.d2h, I.step_done[static_cast<size_t>(s)], 0), "wait");
+        if (timed_copies) ck(cudaEventRecord(I.out_b[static_cast<size_t>(t)], I.d2h), "rec");
         ck(cudaMemcpyAsync(I.host_store[static_cast<size_t>(t)], I.arena + a.offset,
                            static_cast<size_t>(a.bytes), cudaMemcpyDeviceToHost, I.d2h),
            "offload");
+        if (timed_copies) ck(cudaEventRecord(I.out_e[static_cast<size_t>(t)], I.d2h), "rec");
         ck(cudaEventRecord(I.d2h_done[static_cast<size_t>(t)], I.d2h), "record");
+        order.push_back("swap_out fm" + std::to_string(t + 1));
+        timeline.copies.push_back({1, t, 0, 0});
       }
       // completed gradient buckets (every op whose parameters lie in the
       // prefix finished its backward on both streams): all-reduce them (data
@@ -882,6 +948,7 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   } else {
     kernel_launches_ = enqueue_iteration(false);
   }
+  if (!order.empty() || I.graph == nullptr) copy_order_ = order;
   if (next_images && host_inputs) {
     // pipelined input: the next batch's H2D overlaps the rest of this step
     const size_t img3 = sizeof(float) * static_cast<size_t>(k) * cfg_.image * cfg_.image * net.in_c;
@@ -926,6 +993,28 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     }
     st.exposed_swap_ms = exposed;
     trace_ = tr;
+    // real timeline in the simulator's terms (phases and copies, ns)
+    auto ns = [&](cudaEvent_t e) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, I.iter_begin, e), "t");
+      return static_cast<long long>(std::llround(static_cast<double>(ms) * 1e6));
+    };
+    timeline.kstart.assign(static_cast<size_t>(2 * n), 0);
+    timeline.kend.assign(static_cast<size_t>(2 * n), 0);
+    timeline.mem_at_phase.assign(static_cast<size_t>(2 * n), 0);
+    for (int s = 1; s <= 2 * n; ++s) {
+      timeline.kstart[static_cast<size_t>(s - 1)] = ns(I.phase_begin[static_cast<size_t>(s)]);
+      timeline.kend[static_cast<size_t>(s - 1)] = ns(I.phase_end[static_cast<size_t>(s)]);
+      timeline.mem_at_phase[static_cast<size_t>(s - 1)] =
+          static_cast<long long>(fixed_bytes_) + I.lm.live[static_cast<size_t>(s)];
+    }
+    for (auto& c : timeline.copies) {
+      const size_t t = static_cast<size_t>(c.tensor);
+      c.start = ns(c.stream == 1 ? I.out_b[t] : I.in_b[t]);
+      c.end = ns(c.stream == 1 ? I.out_e[t] : I.in_e[t]);
+    }
+    timeline.fixed = fixed_bytes_;
+    timeline_ = timeline;
     if (I.comm && n_buckets > 0) {
       double ar = 0;
       for (int b = 0; b < n_buckets; ++b) {

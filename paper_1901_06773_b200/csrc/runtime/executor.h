@@ -11,9 +11,11 @@
 //     model, the same one the exporter charged to the workspaces;
 //   * a region is reused only after its previous occupant's last reader
 //     (compute event) and drain (D2H event) completed;
-//   * an offload starts when its producing phase's kernels finish; a
-//     prefetch starts `lookahead` phases before its first backward reader
-//     once its offload landed in pinned host memory and its region is free;
+//   * an offload starts when its producing phase's kernels finish; the
+//     prefetches are issued in GMAP order, each as early as the budget
+//     leaves room for its region (the simulator's swap-in queue,
+//     schedule_prefetches), once its offload landed in pinned host memory
+//     and its region is free;
 //   * the whole iteration (kernels, copies, event edges, the bucketed NCCL
 //     all-reduce and the SGD update) can be captured into one CUDA graph.
 #pragma once
@@ -36,6 +38,10 @@ struct ExecConfig {
   unsigned long long budget = 0;   // device cap (hardware.json memory_budget_bytes)
   unsigned long long fixed_allowance = 0;  // m_others + params + grads (planner's fixed)
   int lookahead = 1;
+  // swap-in policy: 1 = the reference runtime's queue (simulator.cpp:113-140,
+  // :233-285): prefetches in GMAP order, each as early as the budget leaves
+  // room (net.h schedule_prefetches); 0 = a fixed `lookahead` phases ahead
+  int prefetch_queue = 1;
   float momentum = 0.9f;
   float weight_decay = 1e-4f;
   float bn_eps = 1e-5f;
@@ -67,6 +73,21 @@ struct ExecConfig {
   // on ResNet-152 k*=42 (1 GPU): 2369 -> 2339 img/s (the update kernels
   // compete with the bandwidth-bound batch norms of the critical path), off
   int overlap_update = 0;
+};
+
+// The real timeline of the last profiled step, for the reference's output
+// documents (exec_capi.cpp serialises it with swapsched's trace_to_csv /
+// mem_curves_csv / stall_bars_csv / summary_to_json)
+struct RealTimeline {
+  std::vector<long long> kstart, kend;  // ns from the iteration start, phases 1..2N
+  struct Copy {
+    int stream = 1;  // 1 = swap_out (D2H), 2 = swap_in (H2D)
+    int tensor = 0;  // featuremap fm_{tensor+1}
+    long long start = 0, end = 0;
+  };
+  std::vector<Copy> copies;               // in stream order
+  std::vector<long long> mem_at_phase;    // fixed + live instance bytes, phases 1..2N
+  unsigned long long fixed = 0;
 };
 
 struct StepStats {
@@ -101,6 +122,11 @@ class Executor {
   void set_comm(const void* nccl_unique_id, int rank, int world);
   bool use_graph = false;
   std::string trace_csv() const { return trace_; }
+  // real timeline of the last profiled step (CUDA events on every phase
+  // and copy), in the reference's simulator terms
+  const RealTimeline& timeline() const { return timeline_; }
+  // the copies of one iteration in stream order ("swap_out fm3", "swap_in fm7", ...)
+  const std::vector<std::string>& copy_order() const { return copy_order_; }
   unsigned long long arena_bytes() const { return arena_bytes_; }
   unsigned long long fixed_bytes() const { return fixed_bytes_; }
   // device bytes NCCL allocated for the communicator (cudaMemGetInfo delta
@@ -114,6 +140,8 @@ class Executor {
   Net net_;
   ExecConfig cfg_;
   std::string trace_;
+  RealTimeline timeline_;
+  std::vector<std::string> copy_order_;
   unsigned long long arena_bytes_ = 0, fixed_bytes_ = 0, comm_bytes_ = 0;
   int kernel_launches_ = 0;
 };

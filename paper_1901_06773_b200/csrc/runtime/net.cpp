@@ -576,6 +576,52 @@ LifetimeModel build_lifetimes(const Net& net, int k, const std::vector<char>& sw
   return lm;
 }
 
+void schedule_prefetches(const Net& net, LifetimeModel& lm, long long cap) {
+  const int n = lm.n;
+  // GMAP order of the prefetches: fm_{t+1} is prefetched in phase 2N - t,
+  // so larger t first
+  std::vector<int> order;
+  for (int t = n - 1; t >= 0; --t) {
+    const int pid = lm.pre_inst[static_cast<size_t>(t)];
+    if (pid >= 0 && lm.inst[static_cast<size_t>(pid)].kind == InstKind::act_prefetched)
+      order.push_back(t);
+  }
+  int prev_first = 1;
+  for (int t : order) {
+    Instance& p = lm.inst[static_cast<size_t>(lm.pre_inst[static_cast<size_t>(t)])];
+    const Instance& a = lm.inst[static_cast<size_t>(lm.act_inst[static_cast<size_t>(t)])];
+    // forward readers use the primary copy: the prefetched one may only
+    // start after them (and after the producer, whose offload it reloads)
+    const int lo = std::max({prev_first, a.last + 1, fwd_step(t) + 1});
+    int s = p.first;
+    while (s - 1 >= lo && lm.live[static_cast<size_t>(s - 1)] + p.bytes <= cap) {
+      --s;
+      lm.live[static_cast<size_t>(s)] += p.bytes;
+    }
+    p.first = s;
+    prev_first = std::max(prev_first, s);
+  }
+  // a prefetch whose first backward reader comes before its GMAP phase (a
+  // block input also read by the downsample convolution) may still start
+  // before its queue predecessors: pull those earlier where the pool has
+  // room, so the swap-in stream issues in GMAP order
+  for (size_t i = order.size(); i-- > 1;) {
+    Instance& p = lm.inst[static_cast<size_t>(lm.pre_inst[static_cast<size_t>(order[i - 1])])];
+    const Instance& q = lm.inst[static_cast<size_t>(lm.pre_inst[static_cast<size_t>(order[i])])];
+    const Instance& a = lm.inst[static_cast<size_t>(lm.act_inst[static_cast<size_t>(order[i - 1])])];
+    const int lo = std::max(a.last + 1, fwd_step(order[i - 1]) + 1);
+    if (q.first >= p.first || q.first < lo) continue;
+    bool fits = true;
+    for (int s = q.first; s < p.first; ++s)
+      fits = fits && lm.live[static_cast<size_t>(s)] + p.bytes <= cap;
+    if (!fits) continue;
+    for (int s = q.first; s < p.first; ++s) lm.live[static_cast<size_t>(s)] += p.bytes;
+    p.first = q.first;
+  }
+  (void)net;
+  lm.peak_bytes = *std::max_element(lm.live.begin(), lm.live.end());
+}
+
 long long plan_arena(LifetimeModel& lm) {
   std::vector<int> order(lm.inst.size());
   std::iota(order.begin(), order.end(), 0);
@@ -590,9 +636,11 @@ long long plan_arena(LifetimeModel& lm) {
   for (int id : order) {
     Instance& x = lm.inst[static_cast<size_t>(id)];
     std::vector<std::pair<long long, long long>> busy;
+    const int xl = std::max(x.last, x.pack_last);
     for (int p : placed) {
       const Instance& y = lm.inst[static_cast<size_t>(p)];
-      if (y.first <= x.last && x.first <= y.last) busy.emplace_back(y.offset, y.offset + y.bytes);
+      if (y.first <= xl && x.first <= std::max(y.last, y.pack_last))
+        busy.emplace_back(y.offset, y.offset + y.bytes);
     }
     std::sort(busy.begin(), busy.end());
     long long off = 0;

@@ -100,6 +100,9 @@ struct Instance {
   long long bytes = 0;     // at the instance's k
   bool swapped = false;    // act: offloaded after production
   long long offset = -1;   // arena offset (executor)
+  // packing lifetime end (>= last): a swapped activation's region may be
+  // kept out of reuse while its offload drains when the budget has room
+  int pack_last = -1;
 };
 
 struct LifetimeModel {
@@ -118,6 +121,16 @@ struct LifetimeModel {
 // H2D prefetch may start before its first backward use
 LifetimeModel build_lifetimes(const Net& net, int k, const std::vector<char>& swapped,
                               int lookahead, long long align);
+
+// The swap-in queue of the reference's runtime model (simulator.cpp:113-140,
+// :233-285) at phase granularity: prefetches are issued in GMAP order (each
+// no earlier than its predecessor in the queue -- head of line), each as
+// early as the pool has room for it until its first backward reader, never
+// before its offload's producer phase has finished with the featuremap.
+// "Room" = live bytes of every instance at each phase + this one <= cap.
+// Moves each prefetched instance's `first` step earlier (never later than
+// the lookahead placement build_lifetimes gave it); recomputes live/peak.
+void schedule_prefetches(const Net& net, LifetimeModel& lm, long long cap);
 
 // static arena offsets: greedy by size, first fit against time-overlapping
 // instances; returns the arena size in bytes

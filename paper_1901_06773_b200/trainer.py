@@ -232,6 +232,13 @@ class Executor:
             if lo < 0 or hi >= self.classes:
                 raise ExecutorError(f"labels outside [0, {self.classes}): [{lo}, {hi}]")
 
+    def document(self, which):
+        """reference-schema documents of the last profiled step: "trace",
+        "mem_curves", "stall_bars", "summary"; "order" = copies in stream order"""
+        p = ctypes.c_void_p()
+        _check(self.lib.accudnn_exec_document(self.h, which.encode(), ctypes.byref(p)), "document")
+        return _take(p.value)
+
     def step(self, images, labels, lr=0.1, update=True, profile=False):
         """images: NCHW float32 [k,3,H,W]; labels int32 [k].  numpy arrays (or
         CPU torch tensors) are copied from host memory inside the step; CUDA

@@ -1,0 +1,138 @@
+"""The swap executor against the reference's runtime model.
+
+simulate_iteration (/root/reference/proj/src/simulator.cpp:79-370) is the
+behavioural contract of the executor: a compute stream running the 2N phases
+in order, a swap-out stream taking the offloads in GMAP order, a swap-in
+stream taking the prefetches in GMAP order, each claiming pool bytes as soon
+as the budget allows (:113-140, :233-285).  Checked here on BASELINE config 1
+(ResNet-20 @ 32, k = 8 by k_override, planner-driven swapping) and a forced
+swap-heavy ResNet-50 plan:
+  * the real copy order per stream equals the simulator's xfer order for the
+    same documents and plan;
+  * the swapping step costs <= 5% over the resident step (exposed swap);
+  * the real timeline is exported in the simulator's document schemas
+    (trace.csv, mem_curves.csv, stall_bars.csv, summary.json).
+"""
+import csv
+import io
+import json
+
+import numpy as np
+import pytest
+
+from paper_1901_06773_b200 import planner, trainer
+
+pytestmark = pytest.mark.gpu
+
+
+def sim_order(net, hw, model, plan, k):
+    _, _, trace = planner.simulate(net, hw, model, plan, "dynamic", k)
+    out = {"swap_out": [], "swap_in": []}
+    for r in csv.DictReader(io.StringIO(trace)):
+        if r["kind"] == "xfer_start" and r["stream"] in out:
+            out[r["stream"]].append(r["subject"])
+    return out
+
+
+def real_order(ex):
+    out = {"swap_out": [], "swap_in": []}
+    for line in ex.document("order").splitlines():
+        stream, obj = line.split()
+        out[stream].append(obj)
+    return out
+
+
+def config(arch, image, classes, cap, k, pins=None):
+    """bench.py's documents for the config; the planner's plan at k (k_override),
+    optionally with a forced pin set ("every3": every third featuremap)"""
+    net, hw, model, desc = trainer.config_documents(arch, image, classes, cap)
+    plan = planner.plan(net, hw, model, k_override=k)
+    if pins == "every3":
+        p = json.loads(plan)
+        p["pinned_objects"] = [f"fm{l}" for l in range(1, len(desc["ops"]) + 1, 3)]
+        plan = json.dumps(p)
+    return net, hw, model, desc, plan
+
+
+def data(k, image, classes, seed):
+    g = np.random.default_rng(seed)
+    return (g.standard_normal((k, 3, image, image)).astype(np.float32),
+            g.integers(0, classes, size=k).astype(np.int32))
+
+
+def timed(ex, x, y, steps=30):
+    ex.set_graph(True)
+    for _ in range(3):
+        ex.step(x, y, lr=0.01)
+    return float(np.median([ex.step(x, y, lr=0.01)["iter_ms"] for _ in range(steps)]))
+
+
+CASES = [("resnet20", 32, 12, 8 << 30, 8, None),      # config 1: the planner's own pins
+         ("resnet50", 64, 8, 8 << 30, 16, "every3")]  # forced swap-heavy plan
+IDS = ["config1-r20", "r50-forced"]
+
+
+@pytest.mark.parametrize("arch,image,classes,cap,k,pins", CASES, ids=IDS)
+def test_copy_order_matches_simulator(cuda_dev, arch, image, classes, cap, k, pins):
+    net, hw, model, desc, plan = config(arch, image, classes, cap, k, pins)
+    ex = trainer.Executor(arch, image, classes, mode="dynamic", plan_json=plan, network_json=net,
+                          hardware_json=hw)
+    ex.set_params(trainer.init_params(desc, 0))
+    x, y = data(k, image, classes, 1)
+    ex.step(x, y, lr=0.01)
+    ex.step(x, y, lr=0.01, update=False, profile=True)
+    real, sim = real_order(ex), sim_order(net, hw, model, plan, k)
+    assert real["swap_out"], "plan swaps nothing"
+    assert real["swap_out"] == sim["swap_out"]
+    assert real["swap_in"] == sim["swap_in"]
+
+
+@pytest.mark.parametrize("arch,image,classes,cap,k,pins", CASES, ids=IDS)
+def test_exposed_swap_within_5_percent(cuda_dev, arch, image, classes, cap, k, pins):
+    """captured step with the plan's swapping vs the same step all resident:
+    the difference is the swap time the copy streams failed to hide"""
+    net, hw, model, desc, plan = config(arch, image, classes, cap, k, pins)
+    params = trainer.init_params(desc, 0)
+    x, y = data(k, image, classes, 2)
+    dyn = trainer.Executor(arch, image, classes, mode="dynamic", plan_json=plan, network_json=net,
+                           hardware_json=hw)
+    res = trainer.Executor(arch, image, classes, k=k, network_json=net, hardware_json=hw)
+    for e in (dyn, res):
+        e.set_params(params)
+    t_res = timed(res, x, y)
+    t_dyn = timed(dyn, x, y)
+    swapped = dyn.step(x, y, lr=0.01, update=False, profile=True)["swapped_bytes"]
+    assert swapped > 0
+    assert t_dyn <= 1.05 * t_res, (t_dyn, t_res, swapped)
+
+
+def test_real_trace_documents(cuda_dev):
+    arch, image, classes, k = "resnet20", 32, 12, 8
+    net, hw, model, desc, plan = config(arch, image, classes, 8 << 30, k)
+    ex = trainer.Executor(arch, image, classes, mode="dynamic", plan_json=plan, network_json=net,
+                          hardware_json=hw)
+    ex.set_params(trainer.init_params(desc, 0))
+    x, y = data(k, image, classes, 3)
+    ex.step(x, y, lr=0.01, update=False, profile=True)
+    n2 = 2 * len(desc["ops"])
+    trace = list(csv.DictReader(io.StringIO(ex.document("trace"))))
+    assert list(trace[0].keys()) == ["time_s", "stream", "kind", "subject", "mem_used_bytes"]
+    starts = [r for r in trace if r["kind"] == "kernel_start"]
+    assert [r["subject"] for r in starts] == [f"phase {j}" for j in range(1, n2 + 1)]
+    times = [float(r["time_s"]) for r in trace]
+    assert times == sorted(times)
+    xin = [r for r in trace if r["stream"] == "swap_in" and r["kind"] == "xfer_start"]
+    landed = {r["subject"]: float(r["time_s"]) for r in trace
+              if r["stream"] == "swap_out" and r["kind"] == "xfer_end"}
+    assert xin
+    for r in xin:  # a prefetch starts only after its offload landed
+        assert float(r["time_s"]) >= landed[r["subject"]]
+    summ = json.loads(ex.document("summary"))
+    assert summ["format_version"] == 1 and not summ["oom"]
+    assert len(summ["per_phase_stall_s"]) == n2
+    bars = list(csv.DictReader(io.StringIO(ex.document("stall_bars"))))
+    assert len(bars) == n2 and list(bars[0].keys()) == ["phase", "stall_s"]
+    curves = ex.document("mem_curves").splitlines()
+    assert curves[0] == "time_s,cum_allocated_bytes,cum_freed_bytes,mem_used_bytes"
+    arena, fixed = ex.memory()
+    assert int(summ["peak_mem_bytes"]) <= arena + fixed <= 8 << 30
