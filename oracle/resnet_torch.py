@@ -46,6 +46,17 @@ class _TF32Conv(torch.autograd.Function):
         return gx, gw, None, None
 
 
+class _Leaves:
+    """the flat parameter vector as the forward pass slices it, backed by one
+    autograd leaf per segment"""
+
+    def __init__(self, leaves):
+        self.leaves = leaves
+
+    def __getitem__(self, sl):
+        return self.leaves[(sl.start, sl.stop)]
+
+
 class TorchResNet:
     """dtype: torch.float32 (default) or torch.float64 (ground truth);
     conv_math: "exact" or "tf32" (emulated tensor-core operand truncation,
@@ -111,20 +122,38 @@ class TorchResNet:
             t[op["id"]] = y
         raise RuntimeError("network without a loss op")
 
+    def _segments(self):
+        segs = []
+        for op in self.ops:
+            if op["kind"] == "conv":
+                segs.append((op["w_off"], op["cout"] * op["r"] * op["r"] * op["cin"]))
+            elif op["kind"] == "fc":
+                segs += [(op["w_off"], op["cout"] * op["cin"]), (op["b_off"], op["cout"])]
+            elif op["kind"] in ("bn", "bn_relu", "bn_add_relu"):
+                segs += [(op["g_off"], op["channels"]), (op["beta_off"], op["channels"])]
+        return segs
+
     def step(self, params, stats, buf, images, labels, lr, momentum=0.9, wd=1e-4,
              first=True, update=True):
-        """One fp32 SGD step on CPU; returns (loss, grads, new_params, new_buf)."""
-        p = torch.tensor(params, dtype=self.dtype, requires_grad=True)
-        loss = self.forward(p, stats.to(self.dtype), torch.as_tensor(images).to(self.dtype),
-                            torch.as_tensor(labels))
+        """One fp32 SGD step on CPU; returns (loss, grads, new_params, new_buf).
+        Every parameter segment is its own autograd leaf (slicing one flat
+        leaf would make each slice's backward materialise a full-size
+        gradient); the flat gradient vector is assembled afterwards."""
+        leaves = {(o, o + n): torch.tensor(params[o:o + n], dtype=self.dtype, requires_grad=True)
+                  for o, n in self._segments()}
+        loss = self.forward(_Leaves(leaves), stats.to(self.dtype),
+                            torch.as_tensor(images).to(self.dtype), torch.as_tensor(labels))
         loss.backward()
-        g = p.grad.detach().numpy().astype(np.float64)
+        g = np.zeros(len(params), dtype=np.float64)
+        for (a, b), t in leaves.items():
+            g[a:b] = t.grad.detach().numpy()
         if not update:
             return loss.item(), g, params, buf
-        w = params.astype(np.float32)
+        ft = np.float64 if self.dtype == torch.float64 else np.float32
+        w = params.astype(ft)
         d = g + wd * w
         nb = d if first else momentum * buf + d
-        return loss.item(), g, (w - lr * nb).astype(np.float32), nb.astype(np.float32)
+        return loss.item(), g, (w - lr * nb).astype(ft), nb.astype(ft)
 
 
 def init_params(describe, seed=0):

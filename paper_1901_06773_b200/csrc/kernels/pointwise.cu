@@ -150,6 +150,11 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
   __syncthreads();
 }
 
+constexpr int kBnPilotRows = 8;
+__device__ __forceinline__ long long bn_pilot_row(long long M, int i) {
+  return M * i / kBnPilotRows;
+}
+
 template <int MODE, bool SKIP>
 __device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c, int lane_r,
                                           long long r_begin, long long r_end, long long step,
@@ -193,17 +198,30 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
   float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0};
   float fsc[4] = {0, 0, 0, 0}, fsh[4] = {0, 0, 0, 0};  // forward scale / shift
-  // forward statistics are accumulated around a per-channel pilot (the
-  // channel's value in row 0, the same for every block): sums of (x - pilot)
-  // and (x - pilot)^2 keep E[x^2] - E[x]^2 free of cancellation when
-  // |mean| >> std (shifted-data variance)
+  // forward statistics are accumulated around a per-channel pilot (the mean
+  // of 8 rows spread over the batch, the same for every block): sums of
+  // (x - pilot) and (x - pilot)^2 keep E[x^2] - E[x]^2 free of cancellation
+  // when |mean| >> std (shifted-data variance).  A single row is not enough:
+  // row 0 is the corner pixel of image 0, which zero padding makes an
+  // outlier of a convolution's output.
   float pil[4] = {0, 0, 0, 0};
   if (MODE == 0 && c_ok && !a.stats_in) {
-    const float4 p4 = __ldg(reinterpret_cast<const float4*>(a.x + c));
-    pil[0] = p4.x;
-    pil[1] = p4.y;
-    pil[2] = p4.z;
-    pil[3] = p4.w;
+#pragma unroll
+    for (int i0 = 0; i0 < kBnPilotRows; i0 += 4) {  // 4 loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        v[i] = __ldg(reinterpret_cast<const float4*>(a.x + bn_pilot_row(a.M, i0 + i) * C + c));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pil[0] += v[i].x;
+        pil[1] += v[i].y;
+        pil[2] += v[i].z;
+        pil[3] += v[i].w;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pil[j] *= 1.f / kBnPilotRows;
   }
   if (MODE == 1 && c_ok) {
 #pragma unroll
@@ -418,7 +436,12 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     const int chn = blockIdx.x * ch + t;
     if (chn < a.C) {
       if (MODE == 0) {
-        const double pilot = a.stats_in ? 0.0 : static_cast<double>(__ldg(a.x + chn));
+        float pf = 0.f;  // the pilot of phase 1, same loads, same order
+        if (!a.stats_in) {
+          for (int i = 0; i < kBnPilotRows; ++i) pf += __ldg(a.x + bn_pilot_row(a.M, i) * C + chn);
+          pf *= 1.f / kBnPilotRows;
+        }
+        const double pilot = static_cast<double>(pf);
         const double dm = s1 / static_cast<double>(a.M);
         const double mean = pilot + dm;
         double var = s2 / static_cast<double>(a.M) - dm * dm;

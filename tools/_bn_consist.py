@@ -1,0 +1,22 @@
+import ctypes, torch, numpy as np, sys, os
+sys.path.insert(0, os.getcwd())
+from paper_1901_06773_b200 import _native
+lib = _native.cuda_lib()
+d = torch.device("cuda")
+P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+for (M, C, shift) in [(4096, 16, 2.0), (4096, 16, 0.0), (1024, 32, 2.0), (256, 64, 2.0), (8192, 256, 2.0)]:
+    g = torch.Generator().manual_seed(1)
+    x = (torch.randn(M, C, generator=g) + shift * torch.randn(C, generator=g)).to(d)
+    gam = (torch.rand(C, generator=g) + 0.5).to(d); bet = (torch.randn(C, generator=g) * 0.1).to(d)
+    y = torch.empty_like(x); mean = torch.empty(C, device=d); inv = torch.empty(C, device=d)
+    ws = torch.zeros(lib.accudnn_bn_workspace_bytes(C) // 4 + 1, device=d)
+    assert lib.accudnn_bn_fwd(P(x), M, C, P(gam), P(bet), 1e-5, 1, P(y), P(mean), P(inv), None, None, 0.1, P(ws), None) == 0
+    torch.cuda.synchronize()
+    sc = gam * inv; sh = bet - mean * sc
+    pre = torch.addcmul(sh, x, sc)  # x*sc + sh (fma-like)
+    yr = torch.relu(x * sc + sh)
+    diff = (y - yr).abs()
+    rows = diff.max(dim=1).values
+    bad = torch.nonzero(rows > 1e-6).flatten()
+    print(M, C, shift, "max|y - relu(x*sc_saved+sh_saved)|", diff.max().item(), "bad rows", bad.numel(),
+          "first", bad[:5].tolist(), "row blocks", sorted(set((bad * 16 // M).tolist()))[:16])
