@@ -15,7 +15,8 @@ from paper_1901_06773_b200 import profiler, trainer  # noqa: E402
 CONFIGS = {
     "resnet152": (224, 1000, 32),
     "resnet50": (224, 1000, 48),
-    "resnet20": (32, 12, 256),
+    # grid 8, 16, 32, 43, 64: config 1 runs at k = 8 (k_override), inside it
+    "resnet20": (32, 12, 64),
     "resnet1001": (32, 12, 32),
 }
 
