@@ -89,6 +89,13 @@ struct Prob {
                        // of the output (the next batch norm's statistics), or nullptr
   int a_packed;        // WGRAD: A stage (4 MN atoms) is one 3-D TMA box
   int b_packed;        // DGRAD: B stage (BN/32 MN atoms) is one 4-D box; WGRAD 1x1: one 3-D box
+  // stream-K (single-CTA tiles): CTA c owns the (tile, k-block) iterations
+  // [c*T/G, (c+1)*T/G) of the tile-major iteration space T = tiles * kb_total;
+  // a tile cut between CTAs leaves one partial per segment in its workspace
+  // block and the last-arriving segment sums them in segment order
+  int streamk;
+  int sk_maxseg;       // segments per tile at most (workspace blocks per tile)
+  unsigned* fix_cnt;   // per-tile arrival counters (zero between launches)
 };
 
 // experiment switch (ACCUDNN_CONV_DRAIN=1): epilogues wait for their bulk
@@ -278,6 +285,15 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
 }
 
 // global output row offset (floats) of GEMM row m
+// stream-K partition: the CTA whose iteration range [c*T/G, (c+1)*T/G)
+// holds iteration x (host and device compute the same)
+__host__ __device__ __forceinline__ int sk_cta_of(long long x, long long T, int G) {
+  int c = static_cast<int>((x * G) / T);
+  while (c + 1 < G && ((c + 1) * T) / G <= x) ++c;
+  while (c > 0 && (c * T) / G > x) --c;
+  return c;
+}
+
 __device__ __forceinline__ long long out_row(const Prob& a, int m) {
   if (!a.scatter) return static_cast<long long>(m) * a.Ng;
   const int hw = a.Hc * a.Wc;
@@ -358,6 +374,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
 
+  // the work of this CTA as a sequence of segments (tile, k-blocks [kb0, kb1));
+  // every role walks the same sequence.  split = the segment's index within
+  // its tile, nseg = the tile's segment count (1: the segment is the tile)
+  constexpr bool kSK = (CM == 1 && BS == 0 && G == 1);
+  const long long sk_T = static_cast<long long>(a.tiles_m) * a.tiles_n * a.kb_total;
+  auto seg_first = [&]() -> long long {
+    return (kSK && a.streamk) ? (static_cast<long long>(cid) * sk_T) / ncl : cid;
+  };
+  const long long sk_end = (static_cast<long long>(cid) + 1) * sk_T / ncl;
+  auto seg_next = [&](long long& pos, int& split, int& tile, int& tm, int& tn, int& kb0, int& kb1,
+                      int& nseg) -> bool {
+    if (kSK && a.streamk) {
+      if (pos >= sk_end) return false;
+      tile = static_cast<int>(pos / a.kb_total);
+      kb0 = static_cast<int>(pos - static_cast<long long>(tile) * a.kb_total);
+      kb1 = static_cast<int>(min(static_cast<long long>(a.kb_total), kb0 + (sk_end - pos)));
+      pos += kb1 - kb0;
+      tm = tile % a.tiles_m;
+      tn = tile / a.tiles_m;
+      const long long t0 = static_cast<long long>(tile) * a.kb_total;
+      const int cf = sk_cta_of(t0, sk_T, ncl);
+      split = cid - cf;
+      nseg = sk_cta_of(t0 + a.kb_total - 1, sk_T, ncl) - cf + 1;
+      return true;
+    }
+    if (pos >= a.units) return false;
+    decode(static_cast<int>(pos), split, tile, tm, tn);
+    kb0 = split * a.kb_per_split;
+    kb1 = min(a.kb_total, kb0 + a.kb_per_split);
+    nseg = a.splits;
+    pos += ncl;
+    return true;
+  };
+  // stream-K fix-up: "this CTA arrived last on the tile" (barrier region)
+  volatile int& s_fix_last = *reinterpret_cast<volatile int*>(tmem_slot + 1);
+
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -420,12 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      for (int u = cid; u < a.units; u += ncl) {
-        int split, tile, tm, tn;
-        decode(u, split, tile, tm, tn);
+      long long pos = seg_first();
+      int split, tile, tm, tn, kb0, kb1, nseg;
+      while (seg_next(pos, split, tile, tm, tn, kb0, kb1, nseg)) {
         const int m0 = tm * kBM, n0 = tn * BN;
-        const int kb0 = split * a.kb_per_split;
-        const int kb1 = min(a.kb_total, kb0 + a.kb_per_split);
         // first output pixel of the tile (FWD: (n,p,q); DGRAD: (n,i,j) of the class grid)
         int pn = 0, pi = 0, pj = 0;
         if constexpr (MODE != WGRAD) {
@@ -579,10 +629,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t kc = 0;
       int j = 0;  // units processed by this CTA
       if (BS && cid < a.units) ptx::mbar_wait(bfull, 0);
-      for (int u = cid; u < a.units; u += ncl, ++j) {
-        const int split = u % a.splits;
-        const int kb0 = split * a.kb_per_split;
-        const int kb1 = min(a.kb_total, kb0 + a.kb_per_split);
+      long long pos = seg_first();
+      int split, tile, tm, tn, kb0, kb1, nseg;
+      for (; seg_next(pos, split, tile, tm, tn, kb0, kb1, nseg); ++j) {
         const int acc = j & 1;
         if (j >= 2) ptx::mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
         ptx::tc_fence_after();
@@ -638,9 +687,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gg = lane & 7;      // read-back 16-byte granule
     uint32_t nchunk = 0;          // chunks staged by this warp (buffer parity)
     int j = 0;
-    for (int u = cid; u < a.units; u += ncl, ++j) {
-      int split, tile, tm, tn;
-      decode(u, split, tile, tm, tn);
+    long long pos = seg_first();
+    int split, tile, tm, tn, kb0, kb1, nseg;
+    for (; seg_next(pos, split, tile, tm, tn, kb0, kb1, nseg); ++j) {
       const int m0 = tm * kBM + quad * 32, n0 = tn * BN;
       const int acc = j & 1;
       ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
@@ -649,7 +698,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t trow = tmem + static_cast<uint32_t>(acc * BN) +
                             (static_cast<uint32_t>(quad * 32) << 16);
       const int ncols = min(BN, a.Ng - n0);  // multiple of 4
-      const bool partial = a.splits > 1;
+      const bool partial = nseg > 1;
+      // stream-K partial: plain stores into the segment's workspace block
+      // [128][BN] (the tile's other segments may still be running)
+      const bool skp = kSK && a.streamk && partial;
+      float* sk_blk = skp ? a.ws + (static_cast<long long>(tile) * a.sk_maxseg + split) * (kBM * BN)
+                          : nullptr;
       const int nch = (ncols + 31) / 32;
 #pragma unroll 1
       for (int ci = 0; ci < nch; ++ci) {
@@ -697,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             a.stats[(P + slot) * a.Ng + col] = cq;
           }
         }
-        if (a.tma_out) {
+        if (a.tma_out && !skp) {
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -725,8 +779,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             d4s[it] = nullptr;
             if (col_ok && m < a.M)
               d4s[it] = reinterpret_cast<float4*>(
-                  partial ? a.ws + (static_cast<long long>(split) * a.M + m) * a.Ng + col
-                          : a.out + out_row(a, m) + col);
+                  skp       ? sk_blk + (m - tm * kBM) * BN + (col - n0)
+                  : partial ? a.ws + (static_cast<long long>(split) * a.M + m) * a.Ng + col
+                            : a.out + out_row(a, m) + col);
             olds[it] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (d4s[it] && a.beta && !partial) olds[it] = __ldcg(d4s[it]);
           }
@@ -757,6 +812,76 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive_cl(mapa_cta0(ptx::smem_u32(&tempty[acc])));
         } else {
           ptx::mbar_arrive(&tempty[acc]);
+        }
+      }
+      if (kSK && skp) {
+        // ---- stream-K fix-up: arrive on the tile; the last segment to
+        // arrive sums the tile's partial blocks in segment order (slot 0 is
+        // the lowest k-blocks), adds the old output for beta = 1 and stores.
+        // Nobody waits for anybody: no assumption about co-resident CTAs.
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64)
+          s_fix_last = atomicAdd(a.fix_cnt + tile, 1u) == static_cast<unsigned>(nseg - 1) ? 1 : 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_fix_last) {
+          __threadfence();
+          const float* blk0 = a.ws + static_cast<long long>(tile) * a.sk_maxseg * (kBM * BN);
+          const int nc4 = ncols >> 2;
+          const int rows = min(kBM, a.M - tm * kBM);
+          const int total = rows * (BN / 4);
+          const int et = threadIdx.x - 64;  // 0..127
+          for (int base = et; base < total; base += 128 * 8) {
+            float4 o[8];
+            int off[8];
+            bool ok[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int f = base + e * 128;
+              const int r = f / (BN / 4), c4 = f - r * (BN / 4);
+              ok[e] = f < total && c4 < nc4;
+              off[e] = r * BN + c4 * 4;
+              o[e] = ok[e] ? __ldcg(reinterpret_cast<const float4*>(blk0 + off[e]))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int sl = 1; sl < nseg; ++sl) {
+              const float* blk = blk0 + static_cast<long long>(sl) * (kBM * BN);
+              float4 p[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                p[e] = ok[e] ? __ldcg(reinterpret_cast<const float4*>(blk + off[e]))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                o[e].x += p[e].x;
+                o[e].y += p[e].y;
+                o[e].z += p[e].z;
+                o[e].w += p[e].w;
+              }
+            }
+            float4* d[8];
+            float4 old[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int r = off[e] / BN;
+              d[e] = ok[e] ? reinterpret_cast<float4*>(a.out + out_row(a, tm * kBM + r) + n0 +
+                                                       (off[e] - r * BN))
+                           : nullptr;
+              if (d[e] && a.beta) old[e] = __ldcg(d[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (d[e]) {
+                if (a.beta) {
+                  o[e].x += old[e].x;
+                  o[e].y += old[e].y;
+                  o[e].z += old[e].z;
+                  o[e].w += old[e].w;
+                }
+                __stcg(d[e], o[e]);
+              }
+          }
+          if (threadIdx.x == 64) a.fix_cnt[tile] = 0u;  // every segment has arrived
         }
       }
       if (a.trace && threadIdx.x == 64 && j < 128) a.trace[blockIdx.x * 1024 + 513 + 2 * j] = clock64();
@@ -1002,12 +1127,29 @@ int g_cur_ctas = 0;
 int cta_slots() { return g_cur_ctas > 0 ? std::min(g_cur_ctas, sm_count()) : sm_count(); }
 long long* g_trace = nullptr;  // debug stamps, see accudnn_conv_trace
 
+// the last kFixBytes of every workspace hold the stream-K per-tile arrival
+// counters (zeroed when the workspace is set, left zero by every launch)
+constexpr size_t kFixBytes = 64 * 1024;
+constexpr int kMaxFixTiles = static_cast<int>(kFixBytes / sizeof(unsigned));
+size_t usable(size_t bytes) { return bytes > 2 * kFixBytes ? bytes - kFixBytes : 0; }
+unsigned* fix_counters(const Workspace& w) {
+  return w.ws && usable(w.bytes)
+             ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(w.ws) + w.bytes - kFixBytes)
+             : nullptr;
+}
+void zero_fix_counters(const Workspace& w) {
+  if (unsigned* c = fix_counters(w)) {
+    cudaMemset(c, 0, kFixBytes);
+    cudaDeviceSynchronize();
+  }
+}
 // lazily owned workspace when the caller did not provide one
 size_t default_ws_capacity() {
   if (!g_ws.ws && !g_ws.bytes && g_ws_default) {
     if (cudaMalloc(&g_ws.ws, g_ws_default) == cudaSuccess) {
       g_ws.bytes = g_ws_default;
       g_ws.owned = true;
+      zero_fix_counters(g_ws);
     } else {
       cudaGetLastError();
       g_ws.ws = nullptr;
@@ -1015,7 +1157,7 @@ size_t default_ws_capacity() {
   }
   return g_ws.ws ? g_ws.bytes : 0;
 }
-size_t ws_capacity() { return g_cur == &g_ws ? default_ws_capacity() : g_cur->bytes; }
+size_t ws_capacity() { return usable(g_cur == &g_ws ? default_ws_capacity() : g_cur->bytes); }
 
 // Split-K factor from a makespan model in SM cycles: a persistent CTA pays
 // a prologue, then waves of units (k-blocks of 2*BN + 128 cycles each plus a
@@ -1135,6 +1277,7 @@ struct Cfg {
   int bn = 0, splits = 0;
   int cm = 1;  // CTAs per cluster sharing the B tile by multicast (1 or 2; FWD / DGRAD)
   int bs = 0;  // B-stationary (FWD / DGRAD, splits 1, cm 1, B tile <= kMaxBStat bytes)
+  int sk = 0;  // stream-K over all CTA slots with the in-kernel fix-up (cm 1, bs 0)
 };
 constexpr size_t kMaxBStat = 128 * 1024;
 struct KeyHash {
@@ -1275,10 +1418,33 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (a.Ng + cfg.bn - 1) / cfg.bn;
   a.splits = cfg.splits;
-  a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
-  a.units = (cfg.cm > 1 ? (a.tiles_m + 1) / 2 : a.tiles_m) * a.tiles_n * a.splits;
   a.ws = g_cur->ws;
   a.trace = g_trace;
+  a.streamk = 0;
+  if (cfg.sk) {
+    // stream-K: G CTAs share the tile-major (tile, k-block) iterations
+    if (cfg.cm != 1 || cfg.bs || a.stats) return -1;
+    const long long tiles = static_cast<long long>(a.tiles_m) * a.tiles_n;
+    const long long T = tiles * a.kb_total;
+    const int G = static_cast<int>(std::min<long long>(T, cta_slots()));
+    if (tiles > kMaxFixTiles || G < 1) return -1;
+    int maxseg = 1;
+    for (long long t = 0; t < tiles; ++t)
+      maxseg = std::max(maxseg, sk_cta_of(t * a.kb_total + a.kb_total - 1, T, G) -
+                                    sk_cta_of(t * a.kb_total, T, G) + 1);
+    if (maxseg > 1 && (static_cast<size_t>(tiles) * maxseg * kBM * cfg.bn * 4 > ws_capacity() ||
+                       !fix_counters(*g_cur)))
+      return -1;
+    a.streamk = 1;
+    a.sk_maxseg = maxseg;
+    a.fix_cnt = fix_counters(*g_cur);
+    a.splits = 1;
+    a.kb_per_split = a.kb_total;
+    a.units = static_cast<int>(std::min<long long>(T, 1 << 30));  // grid = min(T, CTA slots)
+  } else {
+    a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
+    a.units = (cfg.cm > 1 ? (a.tiles_m + 1) / 2 : a.tiles_m) * a.tiles_n * a.splits;
+  }
   // output tensor map for the bulk-store epilogue: the split-K workspace
   // {Ng, M, S} (rows past M clip inside their own slice) or the row-major
   // output {Ng, M}; scatter outputs (strided dgrad classes) store directly
@@ -1355,9 +1521,12 @@ Cfg tune(const Call& c, cudaStream_t st) {
     if (!bn_ok(c, bn)) continue;
     if (bs && static_cast<size_t>(c.a.kb_total) * bn * kBK * 4 > kMaxBStat) continue;
     for (int s : kSplits) {
+     // s = 0: stream-K (single-CTA tiles only)
+     for (int sk : {0, 1}) {
+      if (sk && (s != 1 || cm != 1 || bs)) continue;
       if (!splits_ok(c, s)) continue;
       if (bs && s != 1) continue;
-      const Cfg cand{bn, s, cm, bs};
+      const Cfg cand{bn, s, cm, bs, sk};
       if (launch_cfg(c, cand, st) != 0) {
         cudaGetLastError();
         continue;
@@ -1376,6 +1545,7 @@ Cfg tune(const Call& c, cudaStream_t st) {
         best_ms = t;
         best = cand;
       }
+     }
     }
    }
   }
@@ -1394,10 +1564,18 @@ int run_call(const Call& c, cudaStream_t st) {
     return true;
   }();
   (void)drain_set;
-  if (g_force.bn > 0 || g_force.splits > 0 || g_force.cm > 0) {
+  if (g_force.bn > 0 || g_force.splits != 0 || g_force.cm > 0) {
     Cfg f = model_cfg(c);
     if (g_force.bn > 0 && bn_ok(c, g_force.bn)) f.bn = g_force.bn;
     if (g_force.splits > 0 && splits_ok(c, g_force.splits)) f.splits = g_force.splits;
+    if (g_force.splits == -1) {  // stream-K; falls back where not eligible
+      Cfg k = f;
+      k.splits = 1;
+      k.cm = 1;
+      k.sk = 1;
+      const int r = launch_cfg(c, k, st);
+      if (r != -1) return r;
+    }
     if (g_force.cm > 0) f.cm = g_force.cm == 3 ? 1 : g_force.cm;
     if (g_force.cm == 3) {  // test hook: B-stationary
       f.bs = 1;
@@ -1441,7 +1619,9 @@ int run_call(const Call& c, cudaStream_t st) {
       cfg = model_cfg(c);
     }
   }
-  return launch_cfg(c, cfg, st);
+  int r = launch_cfg(c, cfg, st);
+  if (r == -1 && cfg.sk) r = launch_cfg(c, model_cfg(c), st);  // e.g. a smaller workspace now
+  return r;
 }
 
 void fill_key(Call& c, const accudnn_conv_desc* d, int cls) {
@@ -1622,6 +1802,7 @@ extern "C" int accudnn_conv_set_workspace(void* ptr, unsigned long long bytes) {
   g_ws.bytes = ptr ? static_cast<size_t>(bytes) : 0;
   g_ws.owned = false;
   if (!ptr) g_ws_default = static_cast<size_t>(bytes);
+  zero_fix_counters(g_ws);
   return 0;
 }
 
@@ -1648,6 +1829,7 @@ extern "C" int accudnn_conv_set_stream_workspace(void* stream, void* ptr,
   e->w.ws = static_cast<float*>(ptr);
   e->w.bytes = ptr ? static_cast<size_t>(bytes) : 0;
   e->max_ctas = std::max(0, max_ctas);
+  zero_fix_counters(e->w);
   g_stream_ws.push_back(std::move(e));
   return 0;
 }
@@ -1660,15 +1842,16 @@ extern "C" int accudnn_conv_trace(void* buf) {
   return 0;
 }
 
-// The tuned (BN, splits) table as text, one entry per line:
-// "k0 k1 ... k13 bn splits\n" (the 14-int shape key, see fill_key).  The
+// The tuned table as text, one entry per line:
+// "k0 k1 ... k13 bn splits cm bs sk\n" (the 14-int shape key, see fill_key).  The
 // returned buffer is malloc'ed; release it with free() (accudnn_rt_free).
 extern "C" int accudnn_conv_tune_export(char** out) {
   std::string t;
   for (const auto& kv : accudnn::g_tuned) {
     for (int v : kv.first) t += std::to_string(v) + " ";
     t += std::to_string(kv.second.bn) + " " + std::to_string(kv.second.splits) + " " +
-         std::to_string(kv.second.cm) + " " + std::to_string(kv.second.bs) + "\n";
+         std::to_string(kv.second.cm) + " " + std::to_string(kv.second.bs) + " " +
+         std::to_string(kv.second.sk) + "\n";
   }
   char* buf = static_cast<char*>(std::malloc(t.size() + 1));
   if (!buf) return static_cast<int>(cudaErrorMemoryAllocation);
@@ -1691,6 +1874,7 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     if (!ok) continue;
     if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4)) cfg.cm = 1;
     if (!(ls >> cfg.bs) || (cfg.bs != 0 && cfg.bs != 1)) cfg.bs = 0;
+    if (!(ls >> cfg.sk) || (cfg.sk != 0 && cfg.sk != 1)) cfg.sk = 0;
     if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;
     if (cfg.splits < 1) continue;
     accudnn::g_tuned[key] = cfg;

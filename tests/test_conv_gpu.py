@@ -64,7 +64,7 @@ def check(got, ref):
 
 
 @pytest.fixture(params=["tma", "tma_cluster2", "tma_pair", "tma_pair_bn256_split2", "tma_pair_bn64",
-                        "tma_bn64_split3", "tma_bstat", "cpasync"])
+                        "tma_bn64_split3", "tma_bstat", "tma_streamk", "tma_streamk_bn64", "cpasync"])
 def impl(request):
     """TMA kernel with the analytic config, with the B tile multicast across an
     M-tile pair (cluster of 2), as a CTA pair running 2-SM MMAs (256-row
@@ -84,6 +84,10 @@ def impl(request):
         lib.accudnn_conv_force_cfg(64, 3, 1)
     elif request.param == "tma_bstat":  # B-stationary where the B tile fits, else analytic
         lib.accudnn_conv_force_cfg(64, 0, 3)
+    elif request.param == "tma_streamk":  # stream-K with the in-kernel fix-up
+        lib.accudnn_conv_force_cfg(0, -1, 0)
+    elif request.param == "tma_streamk_bn64":
+        lib.accudnn_conv_force_cfg(64, -1, 0)
     yield request.param
     lib.accudnn_conv_force_cfg(0, 0, 0)
     lib.accudnn_set_conv_impl(1)
@@ -274,3 +278,42 @@ def test_conv_fwd_stats_and_bn_from_stats(cuda_dev, shape, forced):
     assert rel_err(outs[1][1].double(), outs[0][1].double()) < 1e-5
     assert rel_err(outs[1][2].double(), outs[0][2].double()) < 1e-4
     assert rel_err(outs[1][0].double(), outs[0][0].double()) < 1e-4
+
+
+@pytest.mark.parametrize("shape", [(27, 256, 14, 14, 256, 3, 1, 1), (27, 2048, 7, 7, 512, 1, 1, 0),
+                                   (8, 128, 28, 28, 128, 3, 2, 1), (27, 2048, 1, 1, 1000, 1, 1, 0)])
+def test_streamk_deterministic_and_accumulating(cuda_dev, shape):
+    """stream-K: the tile's partial segments are summed in segment order by
+    whichever CTA arrives last, so repeated launches are bit-identical; beta
+    = 1 adds onto the existing output; the per-tile counters return to zero
+    (a following launch is exact again)."""
+    lib = _native.cuda_lib()
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    g = torch.Generator(device=cuda_dev).manual_seed(3)
+    x_d = torch.randn(n, h, w, c, device=cuda_dev, generator=g)
+    w_d = torch.randn(k, r, r, c, device=cuda_dev, generator=g) * 0.05
+    dy_d = torch.randn(n, p, q, k, device=cuda_dev, generator=g)
+    lib.accudnn_conv_force_cfg(0, -1, 0)
+    try:
+        a = (torch.empty(n, p, q, k, device=cuda_dev), torch.empty(n, h, w, c, device=cuda_dev),
+             torch.empty(k, r, r, c, device=cuda_dev))
+        _run_all(lib, d, x_d, w_d, dy_d, a)
+        for _ in range(3):
+            b = tuple(torch.full_like(t, float("nan")) for t in a)
+            torch.randn(1 << 22, device=cuda_dev).sum()  # perturb the schedule
+            _run_all(lib, d, x_d, w_d, dy_d, b)
+            for u, v in zip(a, b):
+                assert torch.equal(u, v)
+        base = torch.randn_like(a[1])
+        acc = base.clone()
+        assert lib.accudnn_conv_dgrad(ctypes.byref(d), dy_d.data_ptr(), w_d.data_ptr(),
+                                      acc.data_ptr(), 1, None) == 0
+        torch.cuda.synchronize()
+        assert torch.allclose(acc, base + a[1], rtol=1e-5, atol=1e-5)
+    finally:
+        lib.accudnn_conv_force_cfg(0, 0, 0)
+    ref = tuple(torch.empty_like(t) for t in a)
+    _run_all(lib, d, x_d, w_d, dy_d, ref)  # default config (split-K / reduce kernel)
+    for u, v in zip(a, ref):
+        assert rel_err(u.double(), v.double()) < 1e-5

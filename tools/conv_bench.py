@@ -1,6 +1,9 @@
 """Times the tcgen05 conv kernels on every distinct ResNet-152 conv shape at
 k images (default 27 = the tuner's k* at 8 GiB) next to cuDNN TF32 (torch,
-channels_last) as a yardstick.  Usage: conv_bench.py [k] [json_out]"""
+channels_last) as a yardstick.  Usage: conv_bench.py [k] [json_out] [mode]
+mode: table (the committed tuned table, default) | retune (autotune every
+shape, candidates include stream-K; the table is written next to json_out)
+| sk (stream-K forced on every launch)"""
 import ctypes
 import json
 import sys
@@ -59,8 +62,13 @@ def main():
     import os
     tune = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "b200",
                         "conv_tune.txt")
-    if os.path.exists(tune):
+    mode_arg = sys.argv[3] if len(sys.argv) > 3 else "table"
+    if mode_arg == "table" and os.path.exists(tune):
         _native.conv_tune_import(open(tune).read())
+    if mode_arg == "retune":
+        lib.accudnn_conv_autotune(1)
+    if mode_arg == "sk":
+        lib.accudnn_conv_force_cfg(0, -1, 0)
     dev = torch.device("cuda:0")
     torch.backends.cudnn.allow_tf32 = True
     torch.backends.cuda.matmul.allow_tf32 = True
@@ -107,6 +115,9 @@ def main():
     print("TOTAL", json.dumps(tot), flush=True)
     if len(sys.argv) > 2:
         json.dump({"k": k, "shapes": out, "total": tot}, open(sys.argv[2], "w"), indent=1)
+        if mode_arg == "retune":
+            with open(sys.argv[2].rsplit(".", 1)[0] + "_tune.txt", "w") as f:
+                f.write(_native.conv_tune_export())
 
 
 if __name__ == "__main__":
