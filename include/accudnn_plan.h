@@ -14,6 +14,9 @@
  *   accudnn_evaluate_k <- evaluate_minibatch (planner.hpp:101-104)
  *   accudnn_kmax       <- max_trainable_minibatch (planner.hpp:60-63)
  *   accudnn_simulate   <- run_simulate   (swapsched.cpp:307-383)
+ *   accudnn_simulate_report <- run_simulate + write_sim_outputs + verify
+ *                            (swapsched.cpp:162-170, 300-383)
+ *   accudnn_with_digest <- with_digest   (swapsched.cpp:114-118)
  *   accudnn_sweep      <- run_sweep      (swapsched.cpp:385-420)
  *   accudnn_tune_lr    <- run_tune_lr    (swapsched.cpp:422-438)
  *   accudnn_generate_fixture <- run_gen  (swapsched.cpp:440-456)
@@ -70,6 +73,21 @@ int accudnn_simulate(const char* network_json, const char* hardware_json,
                      const char* model_json, const char* plan_json,
                      const char* mode, int k, char** summary_json,
                      char** trace_csv);
+
+/* The full `swapsched simulate` output set: summary.json, trace.csv,
+ * mem_curves.csv, stall_bars.csv and (dynamic mode, i.e. with a plan) the
+ * verify_plan document (empty string otherwise).  budget_override != 0
+ * replaces memory_budget_bytes.  rc 1: deadlock or failed verdict. */
+int accudnn_simulate_report(const char* network_json, const char* hardware_json,
+                            const char* model_json, const char* plan_json,
+                            const char* mode, int k, unsigned long long budget_override,
+                            double tolerance, char** summary_json, char** trace_csv,
+                            char** mem_curves_csv, char** stall_bars_csv,
+                            char** verify_json);
+
+/* doc re-serialised with "manifest_digest": digest added (indent 2 + '\n'),
+ * byte-identical to the reference CLI's output files. */
+int accudnn_with_digest(const char* doc, const char* digest, char** out);
 
 int accudnn_sweep(const char* network_json, const char* hardware_json,
                   const char* model_json, const int* k_list, int n_k,

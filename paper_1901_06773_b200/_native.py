@@ -40,6 +40,10 @@ def cuda_lib():
         if not os.path.exists(CUDA_LIB):
             raise NativeMissing(f"{CUDA_LIB} not built; run __graft_entry__.build()")
         planner_lib()  # dependency, resolved through rpath as well
+        # torch first: its bundled libnccl.so.2 (2.28) must be the one the
+        # process maps; libaccudnn's NEEDED libnccl.so.2 then binds to it
+        # instead of the older system copy torch cannot run with.
+        import torch  # noqa: F401
         lib = ctypes.CDLL(CUDA_LIB)
         _declare_cuda(lib)
         _cuda = lib
@@ -78,6 +82,10 @@ PLANNER_SYMBOLS = {
     "simulate": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
                   ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                   ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "simulate_report": ([ctypes.c_char_p] * 5 + [ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double]
+                        + [ctypes.POINTER(ctypes.c_void_p)] * 5, ctypes.c_int),
+    "with_digest": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)],
+                    ctypes.c_int),
     "sweep": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int),
                ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
               ctypes.c_int),

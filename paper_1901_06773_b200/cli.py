@@ -70,9 +70,9 @@ def manifest_digest(subcommand, inputs, params):
 
 
 def _with_digest(doc, digest):
-    j = json.loads(doc)
-    j["manifest_digest"] = digest
-    return json.dumps(j, indent=2) + "\n"
+    """Serialised by the library's JSON writer, as the reference CLI does
+    (swapsched.cpp:114-118): sorted keys, indent 2, trailing newline."""
+    return planner.with_digest(doc, digest)
 
 
 def _cpp_double(x):
@@ -144,22 +144,40 @@ def cmd_plan(a):
     return 0
 
 
+def _write_sim_outputs(out_dir, r, digest):
+    """write_sim_outputs (swapsched.cpp:162-170)."""
+    _write(os.path.join(out_dir, "trace.csv"), r["trace"])
+    _write(os.path.join(out_dir, "summary.json"), _with_digest(r["summary"], digest))
+    _write(os.path.join(out_dir, "mem_curves.csv"), r["mem_curves"])
+    _write(os.path.join(out_dir, "stall_bars.csv"), r["stall_bars"])
+
+
 def cmd_simulate(a):
     inputs = [a.network, a.hardware, a.model] + ([a.plan] if a.plan else [])
     params = [("mode", a.mode), ("k", str(a.k)), ("tolerance", _cpp_double(a.tolerance))]
     if a.budget_bytes:
         params.append(("budget", str(a.budget_bytes)))
+    outs = [os.path.join(a.out_dir, f) for f in
+            ("trace.csv", "summary.json", "mem_curves.csv", "stall_bars.csv")]
+    _forbid_overwrite(inputs, outs)
     digest = manifest_digest("simulate", inputs, params)
     try:
-        rc, summary, trace = planner.simulate(_text(a.network), _text(a.hardware), _text(a.model),
-                                              _text(a.plan) if a.plan else None, a.mode, a.k)
+        rc, r = planner.simulate_report(_text(a.network), _text(a.hardware), _text(a.model),
+                                        _text(a.plan) if a.plan else None, a.mode, a.k,
+                                        budget_override=a.budget_bytes, tolerance=a.tolerance)
     except planner.PlannerError as e:
         raise _map_planner_error(e)
-    _write(os.path.join(a.out_dir, "trace.csv"), trace)
-    _write(os.path.join(a.out_dir, "summary.json"), _with_digest(summary, digest))
-    s = json.loads(summary)
+    _write_sim_outputs(a.out_dir, r, digest)
+    s = json.loads(r["summary"])
+    if s.get("oom"):
+        print(f"oom: {s.get('oom_detail', '')}")
+        return 1
     print("iter_time_s: %.6f" % s.get("iter_time_s", 0.0))
     print("total_stall_s: %.6f" % s.get("total_stall_s", 0.0))
+    print("peak_mem_bytes: %d" % s.get("peak_mem_bytes", 0))
+    if r["verify"]:
+        _write(os.path.join(a.out_dir, "verify.json"), _with_digest(r["verify"], digest))
+        print("verify: %s" % ("pass" if json.loads(r["verify"])["pass"] else "fail"))
     return 1 if rc == 1 else 0
 
 
@@ -194,22 +212,48 @@ def cmd_gen(a):
 
 
 def cmd_pipeline(a):
-    rc = cmd_validate(argparse.Namespace(network=a.network, hardware=a.hardware))
-    if rc:
-        return rc
-    model_path = os.path.join(a.out_dir, "model.json")
-    plan_path = os.path.join(a.out_dir, "plan.json")
-    cmd_fit(argparse.Namespace(network=a.network, profiles=a.profiles, hardware=a.hardware,
-                               eta=a.eta, out=model_path))
-    rc = cmd_plan(argparse.Namespace(network=a.network, hardware=a.hardware, model=model_path,
-                                     step=1, k=0, epochs=1, dataset_size=0, budget_bytes=0,
-                                     out=plan_path))
-    if rc:
-        return rc
-    return cmd_simulate(argparse.Namespace(network=a.network, hardware=a.hardware,
-                                           model=model_path, plan=plan_path, mode="dynamic",
-                                           k=0, tolerance=a.tolerance, budget_bytes=0,
-                                           out_dir=a.out_dir))
+    """validate -> fit -> plan -> simulate -> verify under one manifest digest
+    (run_pipeline, swapsched.cpp:458-533)."""
+    inputs = [a.network, a.hardware] + list(a.profiles)
+    names = ("model.json", "plan.json", "trace.csv", "summary.json", "mem_curves.csv",
+             "stall_bars.csv", "verify.json")
+    _forbid_overwrite(inputs, [os.path.join(a.out_dir, f) for f in names])
+    digest = manifest_digest("pipeline", inputs, [("eta", _cpp_double(a.eta)),
+                                                 ("tolerance", _cpp_double(a.tolerance))])
+    net, hw = _text(a.network), _text(a.hardware)
+    rc, report = planner.validate(net)
+    if rc == 1:
+        for line in (report or "").splitlines():
+            print(f"diagnostic: {line}")
+        return 1
+    print("validate: ok")
+    model = planner.fit(net, [_text(p) for p in a.profiles], hw, eta=a.eta)
+    _write(os.path.join(a.out_dir, "model.json"), _with_digest(model, digest))
+    m = json.loads(model)
+    print("fit: %d curves, bandwidth %.3e B/s" % (len(m.get("curves", [])),
+                                                   m.get("bandwidth_avail_bytes_per_s", 0.0)))
+    try:
+        plan = planner.plan(net, hw, model)
+    except planner.PlannerError as e:
+        if e.code == 1:
+            print(f"plan: {e.message}")
+            return 1
+        raise _map_planner_error(e)
+    _write(os.path.join(a.out_dir, "plan.json"), _with_digest(plan, digest))
+    p = json.loads(plan)
+    print(f"plan: k_star {p['k_star']}, {len(p.get('pinned_objects', []))} pinned")
+    rc, r = planner.simulate_report(net, hw, model, plan, "dynamic", 0, tolerance=a.tolerance)
+    _write_sim_outputs(a.out_dir, r, digest)
+    s = json.loads(r["summary"])
+    if s.get("oom"):
+        print(f"simulate: oom ({s.get('oom_detail', '')})")
+        return 1
+    print("simulate: iter %.6f s, stall %.6f s" % (s.get("iter_time_s", 0.0),
+                                                   s.get("total_stall_s", 0.0)))
+    _write(os.path.join(a.out_dir, "verify.json"), _with_digest(r["verify"], digest))
+    ok = json.loads(r["verify"])["pass"]
+    print("verify: %s" % ("pass" if ok else "fail"))
+    return 0 if ok else 1
 
 
 def cmd_export(a):

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -247,44 +248,123 @@ ABI_EXPORT int ABI(evaluate_k)(const char* network_json, const char* hardware_js
   });
 }
 
+namespace {
+
+// One `swapsched simulate` run (ref: tools/swapsched.cpp:300-383): the
+// outputs write_sim_outputs produces (swapsched.cpp:162-170) plus, with a
+// plan, the verify_plan verdict document.  rc 1: deadlock or failed verdict.
+struct SimRun {
+  std::string summary, trace, mem_curves, stall_bars, verify;
+  bool oom = false;
+  int rc = 0;
+};
+
+SimRun simulate_run(const char* network_json, const char* hardware_json,
+                    const char* model_json, const char* plan_json, const char* mode, int k,
+                    unsigned long long budget_override, double tolerance) {
+  const Loaded L = load(network_json, hardware_json, model_json, budget_override);
+  const SimMode m = mode_from(mode ? mode : "naive");
+  PinSet pins;
+  std::optional<SwapPlan> plan;
+  if (m == SimMode::dynamic) {
+    if (!plan_json) throw SpecError("dynamic mode needs a plan");
+    const json pj = json::parse(plan_json);
+    SwapPlan p;
+    p.k_star = pj.at("k_star").get<int>();
+    for (const auto& name : pj.at("pinned_objects").get<std::vector<std::string>>()) {
+      const auto it = std::find_if(L.gmap.objects.begin(), L.gmap.objects.end(),
+                                   [&](const MemObject& o) { return o.name == name; });
+      if (it == L.gmap.objects.end())
+        throw SpecError("plan pins unknown object '" + name + "'");
+      pins.insert(it->id);
+    }
+    p.pin_set = pins;
+    for (double t : pj.at("t_ready_s").get<std::vector<double>>())
+      p.t_ready.push_back(from_seconds(t));
+    p.predicted_iter_time = from_seconds(pj.at("predicted_iter_time_s").get<double>());
+    plan = std::move(p);
+    if (k <= 0) k = plan->k_star;
+  } else if (m == SimMode::resident) {
+    for (ObjectId id : L.gmap.featuremap_ids()) pins.insert(id);
+  }
+  if (k <= 0) throw SpecError("k is required outside dynamic mode");
+  SimConfig cfg;
+  cfg.budget = L.hw.memory_budget;
+  cfg.fixed_overhead = L.hw.m_others + L.net.param_grad_bytes_total();
+  cfg.mode = m;
+  cfg.bandwidth = L.model.bandwidth_avail;
+  const SimResult sim = simulate_iteration(L.gmap, L.phases, k, pins, L.model, cfg);
+  SimRun r;
+  r.summary = summary_to_json(sim.summary);
+  r.trace = trace_to_csv(sim.events);
+  r.mem_curves = mem_curves_csv(sim.events, cfg.fixed_overhead);
+  r.stall_bars = stall_bars_csv(sim.summary);
+  if (sim.summary.oom) {
+    g_last_error = "oom: " + sim.summary.oom_detail;
+    r.oom = true;
+    r.rc = 1;
+    return r;
+  }
+  if (plan) {
+    const Verdict v = verify_plan(*plan, sim.summary, cfg.budget, tolerance);
+    json vj;
+    vj["format_version"] = 1;
+    vj["pass"] = v.pass;
+    vj["stall_fraction"] = v.stall_fraction;
+    vj["memory_ok"] = v.memory_ok;
+    vj["max_ready_deviation_s"] = to_seconds(v.max_ready_deviation);
+    r.verify = vj.dump(2);
+    if (!v.pass) {
+      g_last_error = "verify: fail (" + v.detail + ")";
+      r.rc = 1;
+    }
+  }
+  return r;
+}
+
+}  // namespace
+
 ABI_EXPORT int ABI(simulate)(const char* network_json, const char* hardware_json,
                              const char* model_json, const char* plan_json,
                              const char* mode, int k, char** summary_json,
                              char** trace_csv) {
   return guarded([&] {
-    const Loaded L = load(network_json, hardware_json, model_json);
-    const SimMode m = mode_from(mode ? mode : "naive");
-    PinSet pins;
-    if (m == SimMode::dynamic) {
-      if (!plan_json) throw SpecError("dynamic mode needs a plan");
-      const json pj = json::parse(plan_json);
-      if (k <= 0) k = pj.at("k_star").get<int>();
-      for (const auto& name : pj.at("pinned_objects").get<std::vector<std::string>>()) {
-        bool found = false;
-        for (const MemObject& o : L.gmap.objects)
-          if (o.name == name) {
-            pins.insert(o.id);
-            found = true;
-            break;
-          }
-        if (!found) throw SpecError("plan pins unknown object '" + name + "'");
-      }
-    } else if (m == SimMode::resident) {
-      for (ObjectId id : L.gmap.featuremap_ids()) pins.insert(id);
-    }
-    if (k <= 0) throw SpecError("k is required outside dynamic mode");
-    SimConfig cfg;
-    cfg.budget = L.hw.memory_budget;
-    cfg.fixed_overhead = L.hw.m_others + L.net.param_grad_bytes_total();
-    cfg.mode = m;
-    cfg.bandwidth = L.model.bandwidth_avail;
-    const SimResult sim = simulate_iteration(L.gmap, L.phases, k, pins, L.model, cfg);
-    put(summary_json, summary_to_json(sim.summary));
-    put(trace_csv, trace_to_csv(sim.events));
-    if (sim.summary.oom) {
-      g_last_error = "oom: " + sim.summary.oom_detail;
-      return 1;
-    }
+    const SimRun r = simulate_run(network_json, hardware_json, model_json, plan_json, mode, k,
+                                  0, 0.02);
+    put(summary_json, r.summary);
+    put(trace_csv, r.trace);
+    // the verdict is not part of this entry point's contract
+    if (!r.oom) g_last_error.clear();
+    return r.oom ? 1 : 0;
+  });
+}
+
+ABI_EXPORT int ABI(simulate_report)(const char* network_json, const char* hardware_json,
+                                    const char* model_json, const char* plan_json,
+                                    const char* mode, int k,
+                                    unsigned long long budget_override, double tolerance,
+                                    char** summary_json, char** trace_csv,
+                                    char** mem_curves_csv_out, char** stall_bars_csv_out,
+                                    char** verify_json) {
+  return guarded([&] {
+    const SimRun r = simulate_run(network_json, hardware_json, model_json, plan_json, mode, k,
+                                  budget_override, tolerance);
+    put(summary_json, r.summary);
+    put(trace_csv, r.trace);
+    put(mem_curves_csv_out, r.mem_curves);
+    put(stall_bars_csv_out, r.stall_bars);
+    put(verify_json, r.verify);
+    return r.rc;
+  });
+}
+
+// with_digest (ref: tools/swapsched.cpp:114-118): the document re-serialised
+// by the JSON library with "manifest_digest" added, indent 2, newline.
+ABI_EXPORT int ABI(with_digest)(const char* doc, const char* digest, char** out) {
+  return guarded([&] {
+    json j = json::parse(doc ? doc : "");
+    j["manifest_digest"] = digest ? digest : "";
+    put(out, j.dump(2) + "\n");
     return 0;
   });
 }

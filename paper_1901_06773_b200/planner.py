@@ -136,6 +136,38 @@ def simulate(network_json, hardware_json, model_json, plan_json=None, mode="dyna
     return rc, s, t
 
 
+def simulate_report(network_json, hardware_json, model_json, plan_json=None, mode="dynamic",
+                    k=0, budget_override=0, tolerance=0.02, *, lib=None, prefix="accudnn_"):
+    """Everything ``swapsched simulate`` writes (swapsched.cpp:300-383).
+
+    Returns (rc, dict) with keys summary, trace, mem_curves, stall_bars and
+    verify (the verify_plan document, "" without a plan); rc 1 means a
+    deadlocked iteration or a failed verdict."""
+    B = _Binding(lib, prefix)
+    outs = [ctypes.c_void_p() for _ in range(5)]
+    rc = B.fn("simulate_report")(*_docs(network_json, hardware_json, model_json),
+                                 _b(plan_json) if plan_json is not None else None, _b(mode),
+                                 int(k), int(budget_override), float(tolerance),
+                                 *[ctypes.byref(o) for o in outs])
+    texts = [B.take(o.value) for o in outs]
+    if rc not in (0, 1) or texts[0] is None:
+        raise PlannerError(rc, B.error())
+    keys = ("summary", "trace", "mem_curves", "stall_bars", "verify")
+    return rc, dict(zip(keys, texts))
+
+
+def with_digest(doc, digest, *, lib=None, prefix="accudnn_"):
+    """The document with "manifest_digest" added, serialised exactly as the
+    reference CLI writes it (swapsched.cpp:114-118)."""
+    B = _Binding(lib, prefix)
+    out = ctypes.c_void_p()
+    rc = B.fn("with_digest")(_b(doc), _b(digest), ctypes.byref(out))
+    text = B.take(out.value)
+    if rc != 0:
+        raise PlannerError(rc, B.error())
+    return text
+
+
 def sweep(network_json, hardware_json, model_json, ks, modes="naive,dynamic,resident",
           parallel=True, *, lib=None, prefix="accudnn_"):
     B = _Binding(lib, prefix)
