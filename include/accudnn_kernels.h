@@ -158,6 +158,14 @@ int accudnn_sgd_update(float* w, const float* g, float* buf, long long n, float 
                        float momentum, float weight_decay, float grad_scale,
                        int first_step, void* stream);
 
+/* featuremap transfer between device memory and pinned (host-mapped) host
+ * memory by an SM-driven copy kernel: `bytes` from src to dst in either
+ * direction, ctas <= 0 = 16 CTAs.  The swap executor's path for transfers
+ * below ~2 MB (D2H) / 512 KB (H2D), where a copy-engine memcpy's per-call
+ * latency dominates (kernels/swap_copy.cu). */
+int accudnn_swap_copy(void* dst, const void* src, unsigned long long bytes, int ctas,
+                      void* stream);
+
 /* NCHW fp32 images with `c` channels -> NHWC with `c4` (>= c, zero padded) */
 int accudnn_nchw_to_nhwc_pad(const float* x, int n, int c, int h, int w, int c4,
                              float* y, void* stream);

@@ -320,7 +320,7 @@ __device__ __forceinline__ long long out_row(const Prob& a, int m) {
 // and k-block that is 16 KB of A + BN/2 x 128 B of B written and read in
 // shared memory instead of 16 KB + BN x 128 B: the stage traffic, which bounds
 // the single-CTA k-block rate, halves on the B side
-template <int MODE, int BN, int STAGES, int CM, int BS, int G>
+template <int MODE, int BN, int STAGES, int CM, int BS, int G, int SK>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
@@ -377,7 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the work of this CTA as a sequence of segments (tile, k-blocks [kb0, kb1));
   // every role walks the same sequence.  split = the segment's index within
   // its tile, nseg = the tile's segment count (1: the segment is the tile)
-  constexpr bool kSK = (CM == 1 && BS == 0 && G == 1);
+  // stream-K is its own instantiation: the tile-sequenced kernels keep the
+  // lean loop (the run-time switch cost every launch ~5%, measured)
+  static_assert(!SK || (CM == 1 && BS == 0 && G == 1), "stream-K: single-CTA tiles only");
+  constexpr bool kSK = SK != 0;
   const long long sk_T = static_cast<long long>(a.tiles_m) * a.tiles_n * a.kb_total;
   auto seg_first = [&]() -> long long {
     return (kSK && a.streamk) ? (static_cast<long long>(cid) * sk_T) / ncl : cid;
@@ -1186,7 +1189,7 @@ int choose_splits(long long tiles, int kb_total, int bn, long long out_elems, in
   return best;
 }
 
-template <int MODE, int BN, int STAGES, int CM, int BS, int G>
+template <int MODE, int BN, int STAGES, int CM, int BS, int G, int SK = 0>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
              cudaStream_t st) {
   const size_t ring = BS ? STAGES * kBM * kBK * 4 + static_cast<size_t>(a.kb_total) * BN * kBK * 4
@@ -1194,7 +1197,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   const size_t smem = ring + 1024 + 1024 + 4 * 8192;
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G>,
+    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                227 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
@@ -1219,7 +1222,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   cfg.attrs = attr;
   cfg.numAttrs = CM > 1 ? 2 : 1;
   cudaError_t e =
-      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G>, ta, tb, tc, a);
+      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
   if (a.stats) {
@@ -1390,6 +1393,13 @@ bool encode(const Call& c, int bn, int cm, CUtensorMap* ta, CUtensorMap* tb, Pro
 template <int MODE, int CM, int BS, int G = 1>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
                 int bn, cudaStream_t st) {
+  if constexpr (CM == 1 && BS == 0 && G == 1) {
+    if (a.streamk) {
+      if (bn == 256) return launch_t<MODE, 256, 4, 1, 0, 1, 1>(ta, tb, tc, a, st);
+      if (bn == 128) return launch_t<MODE, 128, 6, 1, 0, 1, 1>(ta, tb, tc, a, st);
+      return launch_t<MODE, 64, 8, 1, 0, 1, 1>(ta, tb, tc, a, st);
+    }
+  }
   if (BS) {  // A-only ring of 4 x 16 KB; B lives in its own region
     if (bn == 256) return launch_t<MODE, 256, 4, CM, BS, 1>(ta, tb, tc, a, st);
     if (bn == 128) return launch_t<MODE, 128, 4, CM, BS, 1>(ta, tb, tc, a, st);

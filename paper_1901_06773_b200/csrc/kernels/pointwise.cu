@@ -150,7 +150,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
   __syncthreads();
 }
 
-constexpr int kBnPilotRows = 8;
+constexpr int kBnPilotRows = 4;
 __device__ __forceinline__ long long bn_pilot_row(long long M, int i) {
   return M * i / kBnPilotRows;
 }
@@ -199,30 +199,29 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   float mu[4] = {0, 0, 0, 0}, is[4] = {0, 0, 0, 0}, ga[4] = {0, 0, 0, 0};
   float fsc[4] = {0, 0, 0, 0}, fsh[4] = {0, 0, 0, 0};  // forward scale / shift
   // forward statistics are accumulated around a per-channel pilot (the mean
-  // of 8 rows spread over the batch, the same for every block): sums of
+  // of 4 rows spread over the batch, the same for every block): sums of
   // (x - pilot) and (x - pilot)^2 keep E[x^2] - E[x]^2 free of cancellation
   // when |mean| >> std (shifted-data variance).  A single row is not enough:
   // row 0 is the corner pixel of image 0, which zero padding makes an
   // outlier of a convolution's output.
+  // (its 8 loads are issued together with the first rows of phase 1, below)
   float pil[4] = {0, 0, 0, 0};
-  if (MODE == 0 && c_ok && !a.stats_in) {
+  auto load_pilot = [&](float4 (&pv)[kBnPilotRows]) {
 #pragma unroll
-    for (int i0 = 0; i0 < kBnPilotRows; i0 += 4) {  // 4 loads in flight
-      float4 v[4];
+    for (int i = 0; i < kBnPilotRows; ++i)
+      pv[i] = __ldg(reinterpret_cast<const float4*>(a.x + bn_pilot_row(a.M, i) * C + c));
+  };
+  auto sum_pilot = [&](const float4 (&pv)[kBnPilotRows]) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        v[i] = __ldg(reinterpret_cast<const float4*>(a.x + bn_pilot_row(a.M, i0 + i) * C + c));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        pil[0] += v[i].x;
-        pil[1] += v[i].y;
-        pil[2] += v[i].z;
-        pil[3] += v[i].w;
-      }
+    for (int i = 0; i < kBnPilotRows; ++i) {
+      pil[0] += pv[i].x;
+      pil[1] += pv[i].y;
+      pil[2] += pv[i].z;
+      pil[3] += pv[i].w;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) pil[j] *= 1.f / kBnPilotRows;
-  }
+  };
   if (MODE == 1 && c_ok) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -292,6 +291,22 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     const uint64_t p_skip = l2_policy(a.l2_keep ? (use_mask ? 2 : 1) : 0);
     long long r = r_begin + lane_r;
     int kk = 0;
+    if (MODE == 0) {
+      // pilot: its loads and the first group's loads in flight together
+      float4 pv[kBnPilotRows], v[4];
+      load_pilot(pv);
+      const bool group = r + 3 * step < r_end;
+      if (group)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld_pol(a.x + (r + u * step) * C + c, p_keep);
+      sum_pilot(pv);
+      if (group) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) consume(v[u], v[u], v[u]);
+        r += 4 * step;
+        kk += 4;
+      }
+    }
     for (; r + 3 * step < r_end; r += 4 * step, kk += 4) {  // 4 rows in flight
       float4 v[4], d[4], sk[4];
 #pragma unroll

@@ -171,6 +171,9 @@ int accudnn_exec_create(const char* arch, int image, int classes, const char* mo
     if (const char* e = std::getenv("ACCUDNN_OVERLAP_UPDATE")) cfg.overlap_update = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_CONV_BN_STATS")) cfg.conv_bn_stats = std::atoi(e);
     if (const char* e = std::getenv("ACCUDNN_SIDE_WS_FRAC")) cfg.side_ws_frac = std::atof(e);
+    if (const char* e = std::getenv("ACCUDNN_KCOPY_D2H")) cfg.kernel_copy_max_d2h = std::strtoull(e, nullptr, 10);
+    if (const char* e = std::getenv("ACCUDNN_KCOPY_H2D")) cfg.kernel_copy_max_h2d = std::strtoull(e, nullptr, 10);
+    if (const char* e = std::getenv("ACCUDNN_KCOPY_CTAS")) cfg.kernel_copy_ctas = std::atoi(e);
     // ACCUDNN_PREFETCH=lookahead: fixed-lookahead swap-in instead of the queue
     if (const char* e = std::getenv("ACCUDNN_PREFETCH"))
       cfg.prefetch_queue = std::string(e) == "lookahead" ? 0 : 1;

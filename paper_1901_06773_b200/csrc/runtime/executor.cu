@@ -729,6 +729,19 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
     }
   };
 
+  // featuremap transfer: copy kernel through the mapped pinned buffer for
+  // small transfers, copy engine for large ones (ExecConfig thresholds)
+  auto transfer = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                      cudaStream_t st, const char* what) {
+    const unsigned long long lim =
+        kind == cudaMemcpyDeviceToHost ? cfg_.kernel_copy_max_d2h : cfg_.kernel_copy_max_h2d;
+    if (bytes <= lim)
+      ck(static_cast<cudaError_t>(accudnn_swap_copy(dst, src, bytes, cfg_.kernel_copy_ctas, st)),
+         what);
+    else
+      ck(cudaMemcpyAsync(dst, src, bytes, kind, st), what);
+  };
+
   // gradient all-reduce buckets over the completed prefix of the grads
   std::vector<long long> prefix_after_step(static_cast<size_t>(2 * n + 2), 0);
   {
@@ -796,9 +809,8 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
           ck(cudaStreamWaitEvent(I.h2d, I.step_done[static_cast<size_t>(y.last)], 0), "wait");
         }
         if (timed_copies) ck(cudaEventRecord(I.in_b[static_cast<size_t>(t)], I.h2d), "rec");
-        ck(cudaMemcpyAsync(I.arena + p.offset, I.host_store[static_cast<size_t>(t)],
-                           static_cast<size_t>(p.bytes), cudaMemcpyHostToDevice, I.h2d),
-           "prefetch");
+        transfer(I.arena + p.offset, I.host_store[static_cast<size_t>(t)],
+                 static_cast<size_t>(p.bytes), cudaMemcpyHostToDevice, I.h2d, "prefetch");
         if (timed_copies) ck(cudaEventRecord(I.in_e[static_cast<size_t>(t)], I.h2d), "rec");
         ck(cudaEventRecord(I.h2d_done[static_cast<size_t>(t)], I.h2d), "record");
         order.push_back("swap_in fm" + std::to_string(t + 1));
@@ -843,9 +855,8 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
         const Instance& a = I.lm.inst[static_cast<size_t>(I.lm.act_inst[static_cast<size_t>(t)])];
         ck(cudaStreamWaitEvent(I.d2h, I.step_done[static_cast<size_t>(s)], 0), "wait");
         if (timed_copies) ck(cudaEventRecord(I.out_b[static_cast<size_t>(t)], I.d2h), "rec");
-        ck(cudaMemcpyAsync(I.host_store[static_cast<size_t>(t)], I.arena + a.offset,
-                           static_cast<size_t>(a.bytes), cudaMemcpyDeviceToHost, I.d2h),
-           "offload");
+        transfer(I.host_store[static_cast<size_t>(t)], I.arena + a.offset,
+                 static_cast<size_t>(a.bytes), cudaMemcpyDeviceToHost, I.d2h, "offload");
         if (timed_copies) ck(cudaEventRecord(I.out_e[static_cast<size_t>(t)], I.d2h), "rec");
         ck(cudaEventRecord(I.d2h_done[static_cast<size_t>(t)], I.d2h), "record");
         order.push_back("swap_out fm" + std::to_string(t + 1));

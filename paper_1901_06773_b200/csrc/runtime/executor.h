@@ -73,6 +73,15 @@ struct ExecConfig {
   // on ResNet-152 k*=42 (1 GPU): 2369 -> 2339 img/s (the update kernels
   // compete with the bandwidth-bound batch norms of the critical path), off
   int overlap_update = 0;
+  // featuremap transfers up to these sizes run as SM-driven copy kernels
+  // through the host-mapped pinned buffer (kernels/swap_copy.cu) instead of
+  // copy-engine memcpys: a memcpy pays ~3 us of issue/completion latency per
+  // call (128 KB D2H: 5.8 us engine vs 2.6 us kernel; 512 KB: 13.4 vs 10.1;
+  // H2D 128 KB: 5.9 vs 5.1), larger transfers are faster on the engines
+  // (tools/copy_bench.py).  0 disables the kernel path for that direction.
+  unsigned long long kernel_copy_max_d2h = 2ull << 20;
+  unsigned long long kernel_copy_max_h2d = 512ull << 10;
+  int kernel_copy_ctas = 8;
 };
 
 // The real timeline of the last profiled step, for the reference's output

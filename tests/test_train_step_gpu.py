@@ -85,16 +85,20 @@ def assert_fp32_level(desc, loss, g, l64, g64, l32, g32):
       loss: within 3x PyTorch fp32's own deviation from fp64, or 1e-5 relative;
       gradients: the median over parameter tensors of the relative L2 error
       within 3x PyTorch fp32's median, or 2e-5; the whole flat vector within
-      1e-3.  The second bound admits ReLU-mask flips: an element whose
-      pre-activation is within fp32 rounding of 0 (|x| ~ 1e-6) takes the
-      other branch on either side, and its O(1) gradient reaches every
-      earlier layer (observed: one flip in ResNet-20 stage 1 = 3.5e-4)."""
+      3x PyTorch fp32's own deviation of the whole vector, or 1e-3.  The
+      whole-vector bound is relative because ReLU-mask flips make it large
+      for fp32 itself: an element whose pre-activation is within fp32
+      rounding of 0 takes the other branch than in fp64, and its O(1)
+      gradient reaches every earlier layer -- PyTorch's fp32 step deviates
+      from fp64 by 4.0e-2 on ResNet-50 @ 64, k = 8 (tools/fp32_debug.py),
+      the device step by 4.4e-2."""
     e_dev_l, e_ref_l = abs(loss - l64) / abs(l64), abs(l32 - l64) / abs(l64)
     assert e_dev_l <= max(3 * e_ref_l, 1e-5), (e_dev_l, e_ref_l)
     med_dev = float(np.median(tensor_errors(desc, g, g64)))
     med_ref = float(np.median(tensor_errors(desc, g32, g64)))
     assert med_dev <= max(3 * med_ref, 2e-5), (med_dev, med_ref)
-    assert rel(g, g64) <= 1e-3, rel(g, g64)
+    e_dev_g, e_ref_g = rel(g, g64), rel(g32, g64)
+    assert e_dev_g <= max(3 * e_ref_g, 1e-3), (e_dev_g, e_ref_g)
 
 
 @pytest.mark.parametrize("arch,image,classes,k", CASES)
@@ -454,10 +458,12 @@ def test_r152_224_fp32_mode_step_matches_oracles(cuda_dev, precise):
 
 
 def test_r152_224_tf32_sgd_trajectory(cuda_dev):
-    """5 TF32 SGD steps (momentum 0.9, wd 1e-4, lr 0.05) on fresh batches:
+    """5 TF32 SGD steps (momentum 0.9, wd 1e-4, lr 0.002) on fresh batches:
     every step's loss within 2e-2 relative of the TF32-emulating fp32
     oracle's trajectory and of the fp64 trajectory, final parameters within
-    1e-3 relative L2 of the fp64 ones."""
+    1e-3 relative L2 of the fp64 ones.  (At lr 0.05 the k = 2 batch-norm
+    step diverges -- loss 7 -> 51 after one step -- and the trajectory is
+    chaotic for fp32 and fp64 alike.)"""
     arch, image, classes, k = R152
     _, desc = trainer.export_network(arch, image, classes)
     p0 = trainer.init_params(desc, seed=3)
@@ -468,9 +474,9 @@ def test_r152_224_tf32_sgd_trajectory(cuda_dev):
     p_t, p_64, b_t, b_64 = p0.copy(), p0.astype(np.float64), None, None
     for it in range(5):
         x, y = data(k, image, classes, seed=20 + it)
-        dev = ex.step(x, y, lr=0.05)["loss"]
-        lt, _, p_t, b_t = o_t.step(p_t, st_t, b_t, x, y, lr=0.05, first=(it == 0))
-        l64, _, p_64, b_64 = o_64.step(p_64, st_64, b_64, x, y, lr=0.05, first=(it == 0))
+        dev = ex.step(x, y, lr=0.002)["loss"]
+        lt, _, p_t, b_t = o_t.step(p_t, st_t, b_t, x, y, lr=0.002, first=(it == 0))
+        l64, _, p_64, b_64 = o_64.step(p_64, st_64, b_64, x, y, lr=0.002, first=(it == 0))
         assert abs(dev - lt) / abs(lt) < 2e-2, (it, dev, lt, l64)
         assert abs(dev - l64) / abs(l64) < 2e-2, (it, dev, lt, l64)
     assert rel(ex.get_params(), p_64) < 1e-3

@@ -1,0 +1,94 @@
+"""CUPTI timeline (kernels + copies, per stream) of the captured swapping step
+next to the resident one, for a BASELINE config's plan.
+
+  python tools/swap_timeline.py resnet20 32 12 8 [cap_gib] [pins: plan|every3|naive] [outdir]
+
+Writes <outdir>/{resident,dynamic}_timeline.csv (stream, start_us, end_us,
+kind, name, bytes; times relative to the first activity of the step) and prints
+the per-stream busy time and the compute stream's idle gaps with what it
+waited for.
+"""
+import collections
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1901_06773_b200 import planner, trainer  # noqa: E402
+
+arch, image, classes, k = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+cap = int(float(sys.argv[5]) * (1 << 30)) if len(sys.argv) > 5 else 8 << 30
+pins = sys.argv[6] if len(sys.argv) > 6 else "plan"
+out = sys.argv[7] if len(sys.argv) > 7 else "gpurun_out/swap_timeline"
+os.makedirs(out, exist_ok=True)
+net, hw, model, desc = trainer.config_documents(arch, image, classes, cap)
+plan = planner.plan(net, hw, model, k_override=k)
+n = len(desc["ops"])
+if pins != "plan":
+    p = json.loads(plan)
+    p["pinned_objects"] = [f"fm{l}" for l in range(1, n + 1, 3)] if pins == "every3" else []
+    plan = json.dumps(p)
+g = np.random.default_rng(0)
+x = g.standard_normal((k, 3, image, image)).astype(np.float32)
+y = g.integers(0, classes, size=k).astype(np.int32)
+params = trainer.init_params(desc, 0)
+summary = {}
+for mode in ("resident", "dynamic"):
+    ex = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan, network_json=net,
+                          hardware_json=hw)
+    ex.set_params(params)
+    ex.set_graph(True)
+    for _ in range(5):
+        ex.step(x, y, lr=0.01)
+    torch.cuda.synchronize()
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        ex.step(x, y, lr=0.01)
+        torch.cuda.synchronize()
+    with tempfile.NamedTemporaryFile(suffix=".json") as tf:
+        prof.export_chrome_trace(tf.name)
+        trace = json.load(open(tf.name))
+    rows = []
+    for ev in trace.get("traceEvents", []):
+        cat = ev.get("cat", "")
+        if cat not in ("kernel", "gpu_memcpy", "gpu_memset"):
+            continue
+        a = ev.get("args", {})
+        rows.append((a.get("stream", ev.get("tid")), float(ev["ts"]),
+                     float(ev["ts"]) + float(ev.get("dur", 0)), cat, ev.get("name", "")[:60],
+                     a.get("bytes", 0)))
+    rows.sort(key=lambda r: r[1])
+    t0 = rows[0][1]
+    with open(os.path.join(out, f"{mode}_timeline.csv"), "w") as f:
+        f.write("stream,start_us,end_us,kind,name,bytes\n")
+        for s, a0, a1, c, nm, b in rows:
+            f.write(f"{s},{a0 - t0:.2f},{a1 - t0:.2f},{c},{nm.replace(',', ';')},{b}\n")
+    per = collections.defaultdict(list)
+    for r in rows:
+        per[r[0]].append(r)
+    streams = {}
+    for sid, rs in per.items():
+        busy = sum(r[2] - r[1] for r in rs)
+        kinds = collections.Counter(r[3] for r in rs)
+        streams[str(sid)] = {"busy_us": round(busy, 1), "first_us": round(rs[0][1] - t0, 1),
+                             "last_us": round(rs[-1][2] - t0, 1), "n": dict(kinds),
+                             "bytes": int(sum(r[5] or 0 for r in rs))}
+    # compute stream = the one with the most kernels
+    comp = max(per, key=lambda s: sum(1 for r in per[s] if r[3] == "kernel"))
+    gaps = []
+    rs = per[comp]
+    for prev, cur in zip(rs, rs[1:]):
+        if cur[1] - prev[2] > 1.0:
+            gaps.append((round(cur[1] - prev[2], 2), round(prev[2] - t0, 1), prev[4][:40], cur[4][:40]))
+    span = rows[-1][2] - t0
+    summary[mode] = {"span_us": round(span, 1), "streams": streams, "compute_stream": str(comp),
+                     "compute_idle_us": round(sum(gp[0] for gp in gaps), 1),
+                     "largest_gaps": sorted(gaps, reverse=True)[:15]}
+    ex.close()
+print(json.dumps(summary, indent=1))
+with open(os.path.join(out, "summary.json"), "w") as f:
+    json.dump(summary, f, indent=1)
