@@ -102,6 +102,23 @@ int accudnn_generate_fixture(unsigned long long seed, int min_layers,
                              char** hardware_json, char** compute_csv,
                              char** transfer_csv);
 
+/* Incremental re-planning (no reference counterpart; the reference re-plans
+ * from scratch, planner.cpp:346-424).  A session parses the three documents
+ * once and caches, per k, everything Algorithm 2 derives independently of
+ * the device cap and the host-link bandwidth; each accudnn_plan_session_plan
+ * re-runs the search for a new cap (opts->budget_override) and/or bandwidth
+ * (bandwidth_override > 0 replaces bandwidth_avail_bytes_per_s) and writes
+ * the plan.json a fresh accudnn_plan would write for the changed documents.
+ * exact != 0: any opts->step is answered with the step-1 (linear scan)
+ * result.  Errors: accudnn_session_last_error(). */
+const char* accudnn_session_last_error(void);
+int accudnn_plan_session_create(const char* network_json, const char* hardware_json,
+                                const char* model_json, void** session);
+int accudnn_plan_session_plan(void* session, const accudnn_plan_opts* opts,
+                              double bandwidth_override, int exact, char** plan_json);
+int accudnn_plan_session_stats(void* session, long long* hits, long long* misses);
+void accudnn_plan_session_destroy(void* session);
+
 #ifdef __cplusplus
 }
 #endif

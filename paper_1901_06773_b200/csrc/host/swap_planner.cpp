@@ -186,37 +186,46 @@ class PeakTree {
   std::vector<std::int64_t> mx_, lz_;
 };
 
-// Everything evaluate_minibatch needs about one k, computed once.
-struct KContext {
-  const Gmap& g;
-  int k;
-  std::vector<Bytes> sizes;
-  explicit KContext(const Gmap& gm, int kk)
-      : g(gm), k(kk), sizes(detail::scaled_object_sizes(gm, kk)) {}
-};
+}  // namespace
 
-KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases,
-                       int k, const NetworkSpec& net, const HardwareSpec& hw,
-                       const PerfModel& model) {
-  KEvaluation ev;
-  ev.k = k;
-  KContext ctx(g, k);
-  const std::vector<char> none(g.objects.size(), 0);
-  const Bytes fixed = fixed_overhead(net, hw);
-
-  // unpinned running sums (the layer-wise peak with an empty pin set)
-  std::vector<std::int64_t> running(g.ops.size());
-  {
-    std::int64_t s = 0;
-    for (size_t i = 0; i < g.ops.size(); ++i) {
-      const MemOp& op = g.ops[i];
-      s += detail::op_delta(op.kind, static_cast<std::int64_t>(ctx.sizes[op.object]), false);
-      running[i] = s;
-    }
+// Everything about one k that depends on neither the device budget nor the
+// host-link bandwidth (detail::KStatic): k-scaled object sizes, the
+// unpinned running sums and their peak, the 2N phase compute times.
+detail::KStatic detail::make_k_static(const Gmap& g, const std::vector<PhaseLayer>& phases,
+                                      int k, const PerfModel& model) {
+  KStatic st;
+  st.sizes = detail::scaled_object_sizes(g, k);
+  st.running.resize(g.ops.size());
+  std::int64_t s = 0;
+  for (size_t i = 0; i < g.ops.size(); ++i) {
+    const MemOp& op = g.ops[i];
+    s += detail::op_delta(op.kind, static_cast<std::int64_t>(st.sizes[op.object]), false);
+    st.running[i] = s;
   }
   std::int64_t top = 0;
-  for (std::int64_t v : running) top = std::max(top, v);
-  ev.active_area_bytes = static_cast<Bytes>(top);
+  for (std::int64_t v : st.running) top = std::max(top, v);
+  st.top = static_cast<Bytes>(top);
+  return st;
+}
+
+std::vector<TimeNs> detail::k_compute_times(const Gmap& g, const std::vector<PhaseLayer>& phases,
+                                            int k, const PerfModel& model) {
+  std::vector<TimeNs> compute = phase_compute_times(phases, k, model);
+  if (static_cast<int>(compute.size()) != g.num_phases)
+    throw std::invalid_argument("compute_times must cover all 2N phases");
+  return compute;
+}
+
+KEvaluation detail::evaluate_static(const Gmap& g, const KStatic& st, int k,
+                                    const NetworkSpec& net, const HardwareSpec& hw,
+                                    double bandwidth,
+                                    const std::function<const std::vector<TimeNs>&()>& compute_of) {
+  KEvaluation ev;
+  ev.k = k;
+  const std::vector<char> none(g.objects.size(), 0);
+  const Bytes fixed = fixed_overhead(net, hw);
+  const std::vector<Bytes>& sizes = st.sizes;
+  ev.active_area_bytes = st.top;
 
   // C13 memory gate (ref: planner.cpp:261-266)
   if (hw.memory_budget < fixed + ev.active_area_bytes) {
@@ -225,11 +234,11 @@ KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases,
   }
   ev.memory_feasible = true;
 
-  const std::vector<TimeNs> compute = phase_compute_times(phases, k, model);
-  if (static_cast<int>(compute.size()) != g.num_phases)
-    throw std::invalid_argument("compute_times must cover all 2N phases");
+  // compute times only past the memory gate (the reference evaluates them
+  // there, so a model error surfaces at the same k)
+  const std::vector<TimeNs>& compute = compute_of();
   const Bytes available = hw.memory_budget - fixed;
-  ev.t_ready = ready_times(g, ctx.sizes, none, available, model.bandwidth_avail, compute);
+  ev.t_ready = ready_times(g, sizes, none, available, bandwidth, compute);
   ev.omega = stall_violations(ev.t_ready, compute);
   if (ev.omega.empty()) {
     ev.stall_free = true;
@@ -254,7 +263,7 @@ KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases,
     }
   }
   std::sort(cand.begin(), cand.end(), [&](ObjectId a, ObjectId b) {
-    const Bytes sa = ctx.sizes[a], sb = ctx.sizes[b];
+    const Bytes sa = sizes[a], sb = sizes[b];
     return sa != sb ? sa > sb : a < b;
   });
 
@@ -266,12 +275,12 @@ KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases,
   for (size_t i = 0; i < g.ops.size(); ++i) {
     const MemOp& op = g.ops[i];
     if (!is_cand[op.object]) continue;
-    const auto sz = static_cast<std::int64_t>(ctx.sizes[op.object]);
+    const auto sz = static_cast<std::int64_t>(sizes[op.object]);
     if (op.kind == MemOpKind::offload) effect[op.object].emplace_back(i, +sz);
     if (op.kind == MemOpKind::prefetch) effect[op.object].emplace_back(i, -sz);
   }
 
-  PeakTree tree(running);
+  PeakTree tree(st.running);
   Bytes pinned_peak = ev.active_area_bytes;
   std::vector<char> pinned(g.objects.size(), 0);
   for (ObjectId c : cand) {
@@ -280,7 +289,7 @@ KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases,
     if (peak <= available) {
       ev.pins.insert(c);
       pinned[c] = 1;
-      ev.pinned_bytes += ctx.sizes[c];
+      ev.pinned_bytes += sizes[c];
       pinned_peak = peak;
     } else {
       for (const auto& [i, v] : effect[c]) tree.add_suffix(i, -v);
@@ -288,11 +297,23 @@ KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases,
   }
   ev.resident_peak_bytes = pinned_peak;
   if (!ev.pins.empty()) {
-    ev.t_ready = ready_times(g, ctx.sizes, pinned, available, model.bandwidth_avail, compute);
+    ev.t_ready = ready_times(g, sizes, pinned, available, bandwidth, compute);
     ev.omega = stall_violations(ev.t_ready, compute);
   }
   ev.stall_free = ev.omega.empty();
   return ev;
+}
+
+namespace {
+
+KEvaluation evaluate_k(const Gmap& g, const std::vector<PhaseLayer>& phases, int k,
+                       const NetworkSpec& net, const HardwareSpec& hw, const PerfModel& model) {
+  std::vector<TimeNs> compute;
+  return detail::evaluate_static(g, detail::make_k_static(g, phases, k, model), k, net, hw,
+                                 model.bandwidth_avail, [&]() -> const std::vector<TimeNs>& {
+                                   compute = detail::k_compute_times(g, phases, k, model);
+                                   return compute;
+                                 });
 }
 
 // ref: planner.cpp:324-342
@@ -478,14 +499,12 @@ KEvaluation evaluate_minibatch(const Gmap& gmap,
   return evaluate_k(gmap, phases, k, net, hw, model);
 }
 
-// Algorithm 2 (ref: planner.cpp:346-424)
-PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
-                                             const std::vector<PhaseLayer>& phases,
-                                             const NetworkSpec& net,
-                                             const HardwareSpec& hw,
-                                             const PerfModel& model,
-                                             const TrainingConfig& cfg,
-                                             const PlannerOptions& opts) {
+// Algorithm 2 (ref: planner.cpp:346-424) over an evaluator of k
+PlanResult detail::search_plan(const Gmap& gmap, const std::vector<PhaseLayer>& phases,
+                               const NetworkSpec& net, const HardwareSpec& hw,
+                               const PerfModel& model, const TrainingConfig& cfg,
+                               const PlannerOptions& opts,
+                               const std::function<KEvaluation(int)>& evaluate) {
   PlanResult res;
   const KmaxResult km = max_trainable_minibatch(gmap, net, hw);
   if (!km.trainable) {
@@ -495,7 +514,7 @@ PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
   }
 
   if (opts.k_override > 0) {
-    const KEvaluation ev = evaluate_k(gmap, phases, opts.k_override, net, hw, model);
+    const KEvaluation ev = evaluate(opts.k_override);
     if (ev.memory_feasible && ev.stall_free) {
       res.status = PlanStatus::ok;
       res.plan = make_plan(ev, phases, net, hw, model, cfg);
@@ -509,7 +528,7 @@ PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
   }
 
   auto ok_at = [&](int k) {
-    const KEvaluation ev = evaluate_k(gmap, phases, k, net, hw, model);
+    const KEvaluation ev = evaluate(k);
     return ev.memory_feasible && ev.stall_free;
   };
   auto descending = [](int from, int to, int stride) {
@@ -535,7 +554,7 @@ PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
   }
 
   if (!hit) {
-    const KEvaluation one = evaluate_k(gmap, phases, 1, net, hw, model);
+    const KEvaluation one = evaluate(1);
     if (!one.memory_feasible) {
       res.status = PlanStatus::untrainable;
       res.detail = "layer-wise peak at k=1 exceeds the memory budget";
@@ -545,10 +564,22 @@ PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
     }
     return res;
   }
-  const KEvaluation best = evaluate_k(gmap, phases, *hit, net, hw, model);
+  const KEvaluation best = evaluate(*hit);
   res.status = PlanStatus::ok;
   res.plan = make_plan(best, phases, net, hw, model, cfg);
   return res;
+}
+
+PlanResult find_efficiency_optimal_minibatch(const Gmap& gmap,
+                                             const std::vector<PhaseLayer>& phases,
+                                             const NetworkSpec& net,
+                                             const HardwareSpec& hw,
+                                             const PerfModel& model,
+                                             const TrainingConfig& cfg,
+                                             const PlannerOptions& opts) {
+  return detail::search_plan(gmap, phases, net, hw, model, cfg, opts, [&](int k) {
+    return evaluate_k(gmap, phases, k, net, hw, model);
+  });
 }
 
 // ref: planner.cpp:426-433

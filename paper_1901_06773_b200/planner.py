@@ -107,6 +107,65 @@ def plan(network_json, hardware_json, model_json, *, step=1, k_override=0, epoch
     return text
 
 
+class PlanSession:
+    """Incremental re-planning (accudnn_plan_session_*): the documents are
+    parsed once and everything Algorithm 2 derives per k independently of
+    the device cap and the host-link bandwidth is cached, so re-plans for a
+    new cap / bandwidth reuse it.  plan() returns what plan() above returns
+    for the changed documents; exact=True answers any step with the
+    step-1 scan."""
+
+    def __init__(self, network_json, hardware_json, model_json):
+        lib = _native.planner_lib()
+        self._lib = lib
+        lib.accudnn_plan_session_create.argtypes = [ctypes.c_char_p] * 3 + [
+            ctypes.POINTER(ctypes.c_void_p)]
+        lib.accudnn_plan_session_plan.argtypes = [
+            ctypes.c_void_p, ctypes.POINTER(_native.PlanOpts), ctypes.c_double, ctypes.c_int,
+            ctypes.POINTER(ctypes.c_void_p)]
+        lib.accudnn_plan_session_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
+                                                   ctypes.POINTER(ctypes.c_longlong)]
+        lib.accudnn_plan_session_destroy.argtypes = [ctypes.c_void_p]
+        lib.accudnn_plan_session_destroy.restype = None
+        lib.accudnn_session_last_error.restype = ctypes.c_char_p
+        h = ctypes.c_void_p()
+        rc = lib.accudnn_plan_session_create(*_docs(network_json, hardware_json, model_json),
+                                             ctypes.byref(h))
+        if rc != 0:
+            raise PlannerError(rc, lib.accudnn_session_last_error().decode())
+        self._h = h
+
+    def plan(self, *, budget_override=0, bandwidth=0.0, step=1, k_override=0, epochs=1,
+             dataset_size=0, exact=False):
+        opts = _native.PlanOpts(step, k_override, epochs, dataset_size, budget_override)
+        out = ctypes.c_void_p()
+        rc = self._lib.accudnn_plan_session_plan(self._h, ctypes.byref(opts), float(bandwidth),
+                                                 1 if exact else 0, ctypes.byref(out))
+        text = None
+        if out.value:
+            text = ctypes.string_at(out.value).decode()
+            self._lib.accudnn_free(out.value)
+        if rc != 0:
+            raise PlannerError(rc, self._lib.accudnn_session_last_error().decode(), text)
+        return text
+
+    def stats(self):
+        hits, misses = ctypes.c_longlong(), ctypes.c_longlong()
+        self._lib.accudnn_plan_session_stats(self._h, ctypes.byref(hits), ctypes.byref(misses))
+        return {"hits": hits.value, "misses": misses.value}
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.accudnn_plan_session_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def evaluate_k(network_json, hardware_json, model_json, k, *, lib=None, prefix="accudnn_"):
     """One evaluate_minibatch (integer-ns t_ready, pin names) as a dict."""
     B = _Binding(lib, prefix)
