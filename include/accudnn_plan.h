@@ -12,6 +12,7 @@
  *   accudnn_fit        <- run_fit/fit_model (swapsched.cpp:128-137, 193-225)
  *   accudnn_plan       <- run_plan       (swapsched.cpp:241-305)
  *   accudnn_evaluate_k <- evaluate_minibatch (planner.hpp:101-104)
+ *   accudnn_phase_times <- phase_compute_times (perf_model.hpp)
  *   accudnn_kmax       <- max_trainable_minibatch (planner.hpp:60-63)
  *   accudnn_simulate   <- run_simulate   (swapsched.cpp:307-383)
  *   accudnn_simulate_report <- run_simulate + write_sim_outputs + verify
@@ -62,6 +63,11 @@ int accudnn_kmax(const char* network_json, const char* hardware_json,
 int accudnn_plan(const char* network_json, const char* hardware_json,
                  const char* model_json, const accudnn_plan_opts* opts,
                  char** plan_json);
+
+/* the fitted model's 2N phase compute times at minibatch k as CSV
+ * ("phase,time_ns", perf_model.cpp:112-132 phase_compute_times) */
+int accudnn_phase_times(const char* network_json, const char* model_json, int k,
+                        char** times_csv);
 
 /* One KEvaluation as JSON with integer-nanosecond t_ready and pin names. */
 int accudnn_evaluate_k(const char* network_json, const char* hardware_json,

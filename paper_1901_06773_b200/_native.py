@@ -82,6 +82,8 @@ PLANNER_SYMBOLS = {
     "simulate": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
                   ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                   ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "phase_times": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
+                    ctypes.c_int),
     "simulate_report": ([ctypes.c_char_p] * 5 + [ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double]
                         + [ctypes.POINTER(ctypes.c_void_p)] * 5, ctypes.c_int),
     "with_digest": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)],

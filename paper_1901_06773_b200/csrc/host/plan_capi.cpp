@@ -226,6 +226,24 @@ ABI_EXPORT int ABI(plan)(const char* network_json, const char* hardware_json,
   });
 }
 
+// the perf model's 2N phase compute times at k (perf_model.cpp:112-132),
+// one "phase,time_ns" row per phase
+ABI_EXPORT int ABI(phase_times)(const char* network_json, const char* model_json, int k,
+                                char** times_csv) {
+  return guarded([&] {
+    if (!network_json || !model_json) throw std::invalid_argument("network and model required");
+    const NetworkSpec net = parse_network_spec_json(network_json, "network.json");
+    const PerfModel model = perf_model_from_json(model_json, "model.json");
+    const auto phases = unfold_network(net);
+    const auto t = phase_compute_times(phases, k, model);
+    std::string out = "phase,time_ns\n";
+    for (size_t j = 0; j < t.size(); ++j)
+      out += std::to_string(j + 1) + "," + std::to_string(static_cast<long long>(t[j])) + "\n";
+    put(times_csv, out);
+    return 0;
+  });
+}
+
 ABI_EXPORT int ABI(evaluate_k)(const char* network_json, const char* hardware_json,
                                const char* model_json, int k, char** eval_json) {
   return guarded([&] {

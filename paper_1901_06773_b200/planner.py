@@ -107,6 +107,17 @@ def plan(network_json, hardware_json, model_json, *, step=1, k_override=0, epoch
     return text
 
 
+def phase_times(network_json, model_json, k, *, lib=None, prefix="accudnn_"):
+    """The model's 2N phase compute times at k, in integer ns (list)."""
+    B = _Binding(lib, prefix)
+    out = ctypes.c_void_p()
+    rc = B.fn("phase_times")(_b(network_json), _b(model_json), int(k), ctypes.byref(out))
+    text = B.take(out.value)
+    if rc != 0:
+        raise PlannerError(rc, B.error())
+    return [int(line.split(",")[1]) for line in text.splitlines()[1:]]
+
+
 class PlanSession:
     """Incremental re-planning (accudnn_plan_session_*): the documents are
     parsed once and everything Algorithm 2 derives per k independently of

@@ -50,7 +50,11 @@ for k in ks:
                 rows.append({"k": k, "mode": mode, "note": "no plan"})
                 continue
         try:
-            ex = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan)
+            # the same documents as the prediction: the executor's cap and
+            # swap-in queue follow hardware.json (without them a naive plan
+            # falls back to a fixed one-phase prefetch lookahead)
+            ex = trainer.Executor(arch, image, classes, k=k, mode=mode, plan_json=plan,
+                                  network_json=net, hardware_json=hw)
         except Exception as e:  # does not fit the device
             rows.append({"k": k, "mode": mode, "note": str(e)[:80]})
             continue
