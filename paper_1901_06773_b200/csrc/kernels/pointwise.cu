@@ -133,17 +133,26 @@ __device__ __forceinline__ float4 ld_pol(const float* ptr, uint64_t pol) {
 // counters[0] arrivals, counters[1] generation.  (Measured: one barrier over
 // the grid is faster than per-channel-group barriers here.)
 __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblocks) {
-  __threadfence();
+  // bar.sync orders the block's partial writes before thread 0's fence, and
+  // the fence is cumulative: one release fence per block, not per thread
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     volatile unsigned* gen = counters + 1;
     const unsigned g = *gen;
     if (atomicAdd(counters, 1u) == nblocks - 1) {
-      counters[0] = 0u;
-      __threadfence();
+      // release first; the arrival count is reset behind it (one barrier per
+      // launch, so the next arrivals are in the next kernel, after this
+      // store is visible)
       atomicAdd(counters + 1, 1u);
+      counters[0] = 0u;
     } else {
-      while (*gen == g) __nanosleep(64);
+      // poll without sleeping first: the release usually follows within a
+      // few hundred ns, and a sleep's wake-up granularity adds to every
+      // barrier on the critical path
+      int polls = 0;
+      while (*gen == g)
+        if (++polls > 64) __nanosleep(32);
     }
     __threadfence();
   }
@@ -172,6 +181,7 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   __shared__ __align__(16) float cpart[2][kBnGroup];  // CLUSTER: this block's partial
   __shared__ double dsum[kBnThreads];
   __shared__ float coef[6][kBnGroup];
+  __shared__ float pil_s[kBnGroup];  // MODE 0: the phase-1 pilot per channel of the group
   const int lanes = a.lanes;
   const int lane_c = threadIdx.x % lanes;
   const int lane_r = threadIdx.x / lanes;
@@ -193,6 +203,21 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
                         (rows_per_block + rows_per_pass - 1) / rows_per_pass <= 8 * kMaskWords;
   if (use_mask)
     for (int w = 0; w < kMaskWords; ++w) mask_smem[w * kBnThreads + threadIdx.x] = 0u;
+
+  // per-channel parameters phase 2 needs, loaded now so their latency
+  // overlaps phase 1 instead of following the statistics exchange
+  float pre_g = 0.f, pre_b = 0.f, pre_rm = 0.f, pre_rv = 0.f;
+  if (MODE == 0 && static_cast<int>(threadIdx.x) < lanes * 4) {
+    const int chn = blockIdx.x * lanes * 4 + threadIdx.x;
+    if (chn < a.C) {
+      pre_g = a.gamma[chn];
+      pre_b = a.beta[chn];
+      if (blockIdx.y == 0 && a.run_mean && a.run_var) {
+        pre_rm = a.run_mean[chn];
+        pre_rv = a.run_var[chn];
+      }
+    }
+  }
 
   // ---- phase 1: per-block partial sums ----
   float a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
@@ -327,6 +352,9 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       keep_mask(kk, consume(v, d, sk));
     }
   }
+  if (MODE == 0 && c_ok && !a.stats_in && lane_r == 0)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pil_s[lane_c * 4 + j] = pil[j];
   BN_STAMP(1);
   const int gx = gridDim.x;
   float* slot = CLUSTER ? &cpart[0][0]
@@ -421,6 +449,7 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   } else {
     grid_barrier(a.w.counters, gridDim.x * gridDim.y);
+    BN_STAMP(5);
     // ---- phase 2: the group's Y slots, chunked over threads, fixed order ----
     T = kBnThreads / V;
     const int v = threadIdx.x % V;
@@ -451,27 +480,23 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
     const int chn = blockIdx.x * ch + t;
     if (chn < a.C) {
       if (MODE == 0) {
-        float pf = 0.f;  // the pilot of phase 1, same loads, same order
-        if (!a.stats_in) {
-          for (int i = 0; i < kBnPilotRows; ++i) pf += __ldg(a.x + bn_pilot_row(a.M, i) * C + chn);
-          pf *= 1.f / kBnPilotRows;
-        }
+        const float pf = a.stats_in ? 0.f : pil_s[t];  // the pilot of phase 1
         const double pilot = static_cast<double>(pf);
         const double dm = s1 / static_cast<double>(a.M);
         const double mean = pilot + dm;
         double var = s2 / static_cast<double>(a.M) - dm * dm;
         if (var < 0) var = 0;
         const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(a.eps)));
-        const float sc = a.gamma[chn] * inv;
+        const float sc = pre_g * inv;
         coef[0][t] = sc;
-        coef[1][t] = a.beta[chn] - static_cast<float>(mean) * sc;
+        coef[1][t] = pre_b - static_cast<float>(mean) * sc;
         if (blockIdx.y == 0) {
           if (a.save_mean) a.save_mean[chn] = static_cast<float>(mean);
           if (a.save_invstd) a.save_invstd[chn] = inv;
           if (a.run_mean && a.run_var && a.M > 1) {
             const double unbiased = var * static_cast<double>(a.M) / static_cast<double>(a.M - 1);
-            a.run_mean[chn] = (1.f - a.momentum) * a.run_mean[chn] + a.momentum * static_cast<float>(mean);
-            a.run_var[chn] = (1.f - a.momentum) * a.run_var[chn] + a.momentum * static_cast<float>(unbiased);
+            a.run_mean[chn] = (1.f - a.momentum) * pre_rm + a.momentum * static_cast<float>(mean);
+            a.run_var[chn] = (1.f - a.momentum) * pre_rv + a.momentum * static_cast<float>(unbiased);
           }
         }
       } else {
@@ -682,7 +707,20 @@ int bn_launch(BnArgs a, cudaStream_t st) {
   // measured (tools/bn_bench.py, k* = 27 shapes): clusters win for narrow
   // layers with few rows, the cooperative grid for wide or tall ones
   const long long max_blocks = std::min<long long>(static_cast<long long>(occ) * sms, kBnMaxBlocks);
-  const bool cluster = (a.C <= 256 && a.M <= 16LL * 2048) || gx > max_blocks;
+  static int force = -2;  // ACCUDNN_BN_CLUSTER: 1 always, 0 never, unset: measured rule
+  if (force == -2) {
+    const char* e = std::getenv("ACCUDNN_BN_CLUSTER");
+    force = e ? std::atoi(e) : -1;
+  }
+  // measured per mode (tools/bn_bench.py, k* = 42 shapes, forced both ways):
+  // the forward wins with clusters on narrow short layers (14x14x256:
+  // 10.4 vs 11.2 us) and tiny ones; the backward only on tiny ones -- its
+  // cluster variant runs one CTA per SM with spills (14x14x256: 15.6 vs 11.1 us,
+  // residual tail 22.9 vs 14.2 us)
+  bool cluster = a.M < 1024 || gx > max_blocks ||
+                 (MODE == 0 && a.C <= 256 && a.M <= 16LL * 2048);
+  if (force == 1) cluster = true;
+  if (force == 0 && gx <= max_blocks) cluster = false;
   if (cluster) {
     long long y = std::max<long long>(1, (2LL * sms + gx - 1) / gx);
     y = std::min<long long>(y, (a.M + 31) / 32);

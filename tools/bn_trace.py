@@ -38,7 +38,7 @@ lib.accudnn_bn_trace(None)
 t = buf.view(-1, 8).cpu().numpy()
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
-names = ["entry", "phase1 loop", "partial published", "phase2 done", "phase3 done"]
+names = ["entry", "phase1 loop", "partial published", "phase2 done", "phase3 done", "barrier passed"]
 print(f"M={M} C={C} {'bwd' if bwd else 'fwd'} blocks={len(t)}")
 for i, n in enumerate(names):
     col = t[:, i] - t0

@@ -40,7 +40,7 @@ g = np.random.default_rng(0)
 for k in ks:
     x = torch.from_numpy(g.standard_normal((k, 3, image, image)).astype(np.float32)).cuda()
     y = torch.from_numpy(g.integers(0, classes, size=k).astype(np.int32)).cuda()
-    for mode in ("resident", "dynamic", "naive"):
+    for mode in os.environ.get("TABLE1_MODES", "resident,dynamic,naive").split(","):
         p = pred[(k, mode)]
         plan = None
         if mode == "dynamic":
