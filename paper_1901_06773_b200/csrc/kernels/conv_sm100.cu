@@ -320,12 +320,21 @@ __device__ __forceinline__ long long out_row(const Prob& a, int m) {
 // and k-block that is 16 KB of A + BN/2 x 128 B of B written and read in
 // shared memory instead of 16 KB + BN x 128 B: the stage traffic, which bounds
 // the single-CTA k-block rate, halves on the B side
-template <int MODE, int BN, int STAGES, int CM, int BS, int G, int SK>
+template <int MODE, int BN, int STAGES, int CM, int BS, int G, int SK, int KC>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const Prob a) {
   static_assert(G == 1 || (CM == 2 && BS == 0 && MODE != WGRAD), "2-SM tiles: FWD / DGRAD pairs");
+  // KC: split-K across a CTA pair (cluster of 2): CTA rank r accumulates the
+  // k-blocks of half r of the tile in its own TMEM; rank 1 ships its
+  // accumulator chunk by chunk into rank 0's staging buffers through
+  // distributed shared memory, rank 0 adds (slice 0 + slice 1, the fixed
+  // order of the workspace reduction) and stores the tile.  No workspace
+  // round trip, no reduce kernel, and the pair is co-scheduled by hardware.
+  static_assert(!KC || (CM == 1 && BS == 0 && G == 1 && SK == 0 && MODE != WGRAD),
+                "K-split pairs: single-CTA FWD / DGRAD tiles");
+  constexpr int CLS = CM > 1 ? CM : (KC ? 2 : 1);  // cluster size
   constexpr bool kAmn = (MODE == WGRAD);
   constexpr bool kBmn = (MODE != FWD);
   constexpr uint32_t kABytes = kBM * kBK * 4;
@@ -345,17 +354,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained
   uint64_t* bfull = tempty + 2;      // BS: the stationary B tile landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* kc_full = bfull + 1;     // KC rank 0: [warp][slot] peer chunk landed (32 arrivals)
+  uint64_t* kc_empty = kc_full + 8;  // KC rank 1: [warp][slot] rank 0's slot free again
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kc_empty + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 1024 + 768] = gtimer();
-  const uint32_t crank = CM > 1 ? cluster_ctarank() : 0u;
-  const int cid = static_cast<int>(blockIdx.x) / CM;     // cluster index
-  const int ncl = static_cast<int>(gridDim.x) / CM;      // clusters in the grid
+  const uint32_t crank = CLS > 1 ? cluster_ctarank() : 0u;
+  const int cid = static_cast<int>(blockIdx.x) / CLS;    // cluster index
+  const int ncl = static_cast<int>(gridDim.x) / CLS;     // clusters in the grid
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << CM) - 1u);
   // work unit -> (split, m-tile, n-tile); with CM = 2 the unit is a tile pair
   auto decode = [&](int u, int& split, int& tile, int& tm, int& tn) {
+    if constexpr (KC) {  // the unit is a tile; the split is the CTA's rank
+      split = static_cast<int>(crank);
+      tile = u;
+      tm = u % a.tiles_m;
+      tn = u / a.tiles_m;
+      return;
+    }
     split = u % a.splits;
     const int pair = u / a.splits;
     if (BS) {  // the grid is a multiple of tiles_n: u % tiles_n is fixed per CTA
@@ -423,6 +441,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tempty[s], G == 2 ? 2 * (kEpiThreads / 32) : kEpiThreads);
     }
     ptx::mbar_init(bfull, 1);
+    if (KC)
+      for (int i = 0; i < 8; ++i) {
+        ptx::mbar_init(&kc_full[i], 1);
+        ptx::mbar_init(&kc_empty[i], 1);
+      }
     ptx::fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -435,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_alloc<kTmemCols>(tmem_slot);
   }
   ptx::tc_fence_before();
-  if (CM > 1)
+  if (CLS > 1)
     cluster_sync_all();  // peers' barriers initialised before any multicast / remote arrive
   else
     __syncthreads();
@@ -686,6 +709,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;    // staging buffers of this warp
     float* stage_buf = reinterpret_cast<float*>(smem + ring_bytes + 1024) + ew * 2048;
     const uint32_t sbuf0 = ptx::smem_u32(stage_buf);
+    // KC: rank 0's receive slots [warp][2] x 4 KB, after the staging buffers
+    const uint32_t recv0 = ptx::smem_u32(smem + ring_bytes + 1024 + 4 * 8192);
     const int rr_lo = lane >> 3;  // read-back row within a group of 4 (scatter path)
     const int gg = lane & 7;      // read-back 16-byte granule
     uint32_t nchunk = 0;          // chunks staged by this warp (buffer parity)
@@ -701,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t trow = tmem + static_cast<uint32_t>(acc * BN) +
                             (static_cast<uint32_t>(quad * 32) << 16);
       const int ncols = min(BN, a.Ng - n0);  // multiple of 4
-      const bool partial = nseg > 1;
+      const bool partial = nseg > 1 && !KC;
       // stream-K partial: plain stores into the segment's workspace block
       // [128][BN] (the tile's other segments may still be running)
       const bool skp = kSK && a.streamk && partial;
@@ -723,6 +748,75 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const uint32_t sbuf = sbuf0 + (nchunk & 1) * 4096;
+        if constexpr (KC) {
+          // chunk hand-off: rank 1 stages its chunk in its own buffer `sbuf`
+          // and one bulk copy (TMA engine, DSMEM) moves it into rank 0's
+          // receive slot (warp, chunk parity), completing on rank 0's
+          // kc_full; rank 0 frees the slot (kc_empty, remote arrive) as soon
+          // as it has the values in registers, adds its own chunk and stores.
+          // Use u >= 1 of a slot waits for the u-th kc_empty arrival.
+          const int slot = quad * 2 + static_cast<int>(nchunk & 1);
+          const uint32_t use = nchunk >> 1;
+          const uint32_t rslot = recv0 + static_cast<uint32_t>(slot) * 4096;
+          if (crank == 1) {
+            if (use >= 1) ptx::mbar_wait_acq_cluster(&kc_empty[slot], (use - 1) & 1);
+            if (lane == 0) bulk_wait_read<1>();  // our copy out of this buffer has read it
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                               sbuf + lane * 128 + ((g ^ (lane & 7)) << 4)),
+                           "f"(cur[4 * g]), "f"(cur[4 * g + 1]), "f"(cur[4 * g + 2]),
+                           "f"(cur[4 * g + 3])
+                           : "memory");
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              uint32_t rbuf, rbar;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rbuf) : "r"(rslot));
+              asm volatile("mapa.shared::cluster.u32 %0, %1, 0;"
+                           : "=r"(rbar)
+                           : "r"(ptx::smem_u32(&kc_full[slot])));
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
+                  " [%0], [%1], 4096, [%2];" ::"r"(rbuf),
+                  "r"(sbuf), "r"(rbar)
+                  : "memory");
+              bulk_commit();
+            }
+            ++nchunk;
+            continue;
+          }
+          if (lane == 0) mbar_expect_tx(&kc_full[slot], 4096);  // arm this use
+          ptx::mbar_wait(&kc_full[slot], use & 1);
+          float peer[32];
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(peer[4 * g]), "=f"(peer[4 * g + 1]), "=f"(peer[4 * g + 2]),
+                           "=f"(peer[4 * g + 3])
+                         : "r"(rslot + lane * 128 + ((g ^ (lane & 7)) << 4))
+                         : "memory");
+          __syncwarp();
+          if (lane == 0) {  // the slot's values are in registers: hand it back
+            uint32_t pe;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 1;"
+                         : "=r"(pe)
+                         : "r"(ptx::smem_u32(&kc_empty[slot])));
+            mbar_arrive_cl(pe);
+            bulk_wait_read<1>();  // our store that used `sbuf` has read it
+          }
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 32; ++g) cur[g] += peer[g];  // slice 0 + slice 1
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             sbuf + lane * 128 + ((g ^ (lane & 7)) << 4)),
+                         "f"(cur[4 * g]), "f"(cur[4 * g + 1]), "f"(cur[4 * g + 2]),
+                         "f"(cur[4 * g + 3])
+                         : "memory");
+        } else {
         if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
         __syncwarp();
 #pragma unroll
@@ -731,6 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            sbuf + lane * 128 + ((g ^ (lane & 7)) << 4)),
                        "f"(cur[4 * g]), "f"(cur[4 * g + 1]), "f"(cur[4 * g + 2]), "f"(cur[4 * g + 3])
                        : "memory");
+        }
         if (a.stats && !partial) {
           // column sums of this 32x32 chunk for the next batch norm: lane l
           // walks column l of the staged (swizzled) chunk; rows past M skipped
@@ -900,8 +995,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   ptx::tc_fence_before();
-  if (CM > 1)
-    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
+  if (CLS > 1)
+    cluster_sync_all();  // no CTA leaves while its peer may still write / arrive into it
   else
     __syncthreads();
   if (warp == 1) {
@@ -1189,22 +1284,23 @@ int choose_splits(long long tiles, int kb_total, int bn, long long out_elems, in
   return best;
 }
 
-template <int MODE, int BN, int STAGES, int CM, int BS, int G, int SK = 0>
+template <int MODE, int BN, int STAGES, int CM, int BS, int G, int SK = 0, int KC = 0>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
              cudaStream_t st) {
   const size_t ring = BS ? STAGES * kBM * kBK * 4 + static_cast<size_t>(a.kb_total) * BN * kBK * 4
                          : STAGES * (kBM + BN / G) * kBK * 4;
-  const size_t smem = ring + 1024 + 1024 + 4 * 8192;
+  const size_t smem = ring + 1024 + 1024 + 4 * 8192 + (KC ? 4 * 8192 : 0);
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK>,
+    const cudaError_t e = cudaFuncSetAttribute(conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK, KC>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                227 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
     configured = true;
   }
   if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidValue);
-  int grid = CM * static_cast<int>(std::min<long long>(a.units, cta_slots() / CM));
+  constexpr int CLS = CM > 1 ? CM : (KC ? 2 : 1);
+  int grid = CLS * static_cast<int>(std::min<long long>(a.units, cta_slots() / CLS));
   if (BS) grid = std::min(cta_slots(), a.units) / a.tiles_n * a.tiles_n;  // fixed N-tile per CTA
   if (grid < 1) return static_cast<int>(cudaErrorInvalidValue);
   cudaLaunchConfig_t cfg = {};
@@ -1216,15 +1312,15 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = CM;
+  attr[1].val.clusterDim.x = CLS;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = CM > 1 ? 2 : 1;
+  cfg.numAttrs = CLS > 1 ? 2 : 1;
   cudaError_t e =
-      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK>, ta, tb, tc, a);
+      cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK, KC>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess || a.splits == 1) return static_cast<int>(e);
+  if (e != cudaSuccess || a.splits == 1 || KC) return static_cast<int>(e);
   if (a.stats) {
     const long long blocks = (static_cast<long long>(a.M) + 31) / 32 * (a.Ng / 32);
     const int rgrid = static_cast<int>(std::min<long long>(blocks, 16LL * sm_count()));
@@ -1415,10 +1511,26 @@ int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   return launch_t<MODE, 64, 8, CM, BS, 1>(ta, tb, tc, a, st);
 }
 
+template <int MODE>
+int dispatch_kc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Prob& a,
+                int bn, cudaStream_t st) {
+  // one ring stage fewer than the plain kernels: the receive slots take 32 KB
+  if (bn == 256) return launch_t<MODE, 256, 3, 1, 0, 1, 0, 1>(ta, tb, tc, a, st);
+  if (bn == 128) return launch_t<MODE, 128, 5, 1, 0, 1, 0, 1>(ta, tb, tc, a, st);
+  return launch_t<MODE, 64, 6, 1, 0, 1, 0, 1>(ta, tb, tc, a, st);
+}
+
 // -1: could not encode the tensor maps (not launched)
 int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   CUtensorMap ta, tb;
   Prob a = c.a;
+  // cm 5: split-K over a CTA pair, reduced through DSMEM (FWD / DGRAD,
+  // row-major outputs written by the bulk-store epilogue, 2 slices)
+  const bool kc = cfg.cm == 5;
+  if (kc) {
+    if (c.mode == WGRAD || cfg.splits != 2 || cfg.bs || cfg.sk || a.scatter || a.stats) return -1;
+    cfg.cm = 1;
+  }
   if (c.mode == WGRAD) cfg.cm = 1;  // multicast of B across M-tiles: FWD / DGRAD only
   if (cfg.bs && (c.mode == WGRAD || cfg.splits != 1 || cfg.cm != 1 ||
                  static_cast<size_t>(c.a.kb_total) * cfg.bn * kBK * 4 > kMaxBStat))
@@ -1451,6 +1563,10 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
     a.splits = 1;
     a.kb_per_split = a.kb_total;
     a.units = static_cast<int>(std::min<long long>(T, 1 << 30));  // grid = min(T, CTA slots)
+  } else if (kc) {
+    a.kb_per_split = (a.kb_total + 1) / 2;
+    if (a.kb_per_split >= a.kb_total) return -1;  // one k-block: nothing to split
+    a.units = a.tiles_m * a.tiles_n;  // per CTA pair
   } else {
     a.kb_per_split = (a.kb_total + a.splits - 1) / a.splits;
     a.units = (cfg.cm > 1 ? (a.tiles_m + 1) / 2 : a.tiles_m) * a.tiles_n * a.splits;
@@ -1461,7 +1577,7 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   CUtensorMap tc;
   std::memset(&tc, 0, sizeof(tc));
   a.tma_out = 0;
-  if (a.splits > 1) {
+  if (a.splits > 1 && !kc) {
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.Ng), static_cast<cuuint64_t>(a.M),
                                 static_cast<cuuint64_t>(a.splits)};
     const cuuint64_t str[2] = {static_cast<cuuint64_t>(a.Ng) * 4,
@@ -1475,6 +1591,11 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
     a.tma_out = tiled_map(&tc, a.out, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
   }
   if (cfg.bs && a.tiles_n > sm_count()) cfg.bs = 0;
+  if (kc) {
+    if (!a.tma_out) return -1;
+    return c.mode == FWD ? dispatch_kc<FWD>(ta, tb, tc, a, cfg.bn, st)
+                         : dispatch_kc<DGRAD>(ta, tb, tc, a, cfg.bn, st);
+  }
   if (c.mode == FWD)
     return cfg.bs ? dispatch_bn<FWD, 1, 1>(ta, tb, tc, a, cfg.bn, st)
            : cfg.cm == 4 ? dispatch_bn<FWD, 2, 0, 2>(ta, tb, tc, a, cfg.bn, st)
@@ -1523,8 +1644,9 @@ Cfg tune(const Call& c, cudaStream_t st) {
   float best_ms = 1e30f;
   // 0: plain, 1: 2-CTA multicast, 3: 2-SM MMA pair.  (2, B-stationary, is
   // available through accudnn_conv_force_cfg but not tuned: measured no faster)
-  for (int variant : {0, 1, 3}) {
-   const int cm = variant == 1 ? 2 : variant == 3 ? 4 : 1;
+  // 5: split-K over a DSMEM-reduced CTA pair (2 slices)
+  for (int variant : {0, 1, 3, 5}) {
+   const int cm = variant == 1 ? 2 : variant == 3 ? 4 : variant == 5 ? 5 : 1;
    const int bs = variant == 2 ? 1 : 0;
    if (variant > 0 && c.mode == WGRAD) continue;
    for (int bn : {64, 128, 256}) {
@@ -1534,6 +1656,7 @@ Cfg tune(const Call& c, cudaStream_t st) {
      // s = 0: stream-K (single-CTA tiles only)
      for (int sk : {0, 1}) {
       if (sk && (s != 1 || cm != 1 || bs)) continue;
+      if (cm == 5 && (s != 2 || sk)) continue;
       if (!splits_ok(c, s)) continue;
       if (bs && s != 1) continue;
       const Cfg cand{bn, s, cm, bs, sk};
@@ -1590,6 +1713,14 @@ int run_call(const Call& c, cudaStream_t st) {
     if (g_force.cm == 3) {  // test hook: B-stationary
       f.bs = 1;
       f.splits = 1;
+    }
+    if (g_force.cm == 5) {  // test hook: split-K pair reduced through DSMEM
+      f.splits = 2;
+      f.bs = 0;
+      f.sk = 0;
+      const int r = launch_cfg(c, f, st);
+      if (r != -1) return r;
+      f = model_cfg(c);  // not eligible (WGRAD, scatter output, one k-block)
     }
     return launch_cfg(c, f, st);
   }
@@ -1882,7 +2013,7 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     for (int& v : key) ok = ok && static_cast<bool>(ls >> v);
     ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
     if (!ok) continue;
-    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4)) cfg.cm = 1;
+    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4 && cfg.cm != 5)) cfg.cm = 1;
     if (!(ls >> cfg.bs) || (cfg.bs != 0 && cfg.bs != 1)) cfg.bs = 0;
     if (!(ls >> cfg.sk) || (cfg.sk != 0 && cfg.sk != 1)) cfg.sk = 0;
     if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;

@@ -33,6 +33,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// wait with cluster-scope acquire: the phase was completed by arrivals
+// (mbarrier.arrive.release.cluster) of another CTA of the cluster, whose
+// preceding distributed-shared-memory writes become visible here
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // ---- cp.async (LDGSTS) -------------------------------------------------------
 // 16-byte copy; src_bytes == 0 zero-fills the destination (padding / tails)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {

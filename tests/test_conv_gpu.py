@@ -64,7 +64,8 @@ def check(got, ref):
 
 
 @pytest.fixture(params=["tma", "tma_cluster2", "tma_pair", "tma_pair_bn256_split2", "tma_pair_bn64",
-                        "tma_bn64_split3", "tma_bstat", "tma_streamk", "tma_streamk_bn64", "cpasync"])
+                        "tma_bn64_split3", "tma_bstat", "tma_streamk", "tma_streamk_bn64",
+                        "tma_kpair", "tma_kpair_bn256", "tma_kpair_bn64", "cpasync"])
 def impl(request):
     """TMA kernel with the analytic config, with the B tile multicast across an
     M-tile pair (cluster of 2), as a CTA pair running 2-SM MMAs (256-row
@@ -88,6 +89,12 @@ def impl(request):
         lib.accudnn_conv_force_cfg(0, -1, 0)
     elif request.param == "tma_streamk_bn64":
         lib.accudnn_conv_force_cfg(64, -1, 0)
+    elif request.param == "tma_kpair":  # split-K over a CTA pair, reduced through DSMEM
+        lib.accudnn_conv_force_cfg(0, 0, 5)
+    elif request.param == "tma_kpair_bn256":
+        lib.accudnn_conv_force_cfg(256, 0, 5)
+    elif request.param == "tma_kpair_bn64":
+        lib.accudnn_conv_force_cfg(64, 0, 5)
     yield request.param
     lib.accudnn_conv_force_cfg(0, 0, 0)
     lib.accudnn_set_conv_impl(1)
@@ -317,3 +324,54 @@ def test_streamk_deterministic_and_accumulating(cuda_dev, shape):
     _run_all(lib, d, x_d, w_d, dy_d, ref)  # default config (split-K / reduce kernel)
     for u, v in zip(a, ref):
         assert rel_err(u.double(), v.double()) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(27, 256, 14, 14, 256, 3, 1, 1), (42, 256, 14, 14, 256, 3, 1, 1),
+                                   (42, 1024, 14, 14, 256, 1, 1, 0), (42, 256, 14, 14, 1024, 1, 1, 0),
+                                   (42, 512, 7, 7, 512, 3, 1, 1), (3, 96, 10, 10, 160, 3, 1, 1)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_kpair_equals_two_slice_workspace_reduction(cuda_dev, shape, bn):
+    """The DSMEM-reduced split-K pair (cm 5) computes slice 0 + slice 1 of the
+    same k-block partition as the 2-slice workspace path (splits 2), so both
+    are bit-identical, for overwrite and for accumulation (beta = 1), on the
+    forward and the data gradient; repeated launches are bit-identical."""
+    lib = _native.cuda_lib()
+    n, c, h, w, k, r, stride, pad = shape
+    d, p, q = desc(*shape)
+    g = torch.Generator(device=cuda_dev).manual_seed(5)
+    x_d = torch.randn(n, h, w, c, device=cuda_dev, generator=g)
+    w_d = torch.randn(k, r, r, c, device=cuda_dev, generator=g) * 0.05
+    dy_d = torch.randn(n, p, q, k, device=cuda_dev, generator=g)
+    base_y = torch.randn(n, p, q, k, device=cuda_dev, generator=g)
+    base_x = torch.randn(n, h, w, c, device=cuda_dev, generator=g)
+
+    def run(cm):
+        lib.accudnn_conv_force_cfg(bn, 2, cm)
+        try:
+            y, dx = torch.full_like(base_y, float("nan")), torch.full_like(base_x, float("nan"))
+            ya, dxa = base_y.clone(), base_x.clone()
+            for out, beta in ((y, 0), (ya, 1)):
+                assert lib.accudnn_conv_fwd(ctypes.byref(d), x_d.data_ptr(), w_d.data_ptr(),
+                                            out.data_ptr(), beta, None) == 0
+            for out, beta in ((dx, 0), (dxa, 1)):
+                assert lib.accudnn_conv_dgrad(ctypes.byref(d), dy_d.data_ptr(), w_d.data_ptr(),
+                                              out.data_ptr(), beta, None) == 0
+            torch.cuda.synchronize()
+            return y, ya, dx, dxa
+        finally:
+            lib.accudnn_conv_force_cfg(0, 0, 0)
+
+    # the 2-slice workspace path needs 2 x M x N floats of workspace
+    lib.accudnn_conv_set_workspace(None, ctypes.c_ulonglong(512 << 20))
+    try:
+        ws = run(1)
+    finally:
+        lib.accudnn_conv_set_workspace(None, ctypes.c_ulonglong(64 << 20))
+    kp = run(5)
+    again = run(5)
+    for u, v, t in zip(ws, kp, again):
+        assert torch.equal(u, v)
+        assert torch.equal(v, t)
+    ref = F.conv2d(x_d.permute(0, 3, 1, 2).double().cpu(), w_d.permute(0, 3, 1, 2).double().cpu(),
+                   stride=stride, padding=pad)
+    check(kp[0].permute(0, 3, 1, 2), ref)
