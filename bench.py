@@ -438,6 +438,10 @@ def run_ours(args):
     # (every rank plans on identical documents: identical k* and pins; N > 1
     # charges NCCL's device buffers to the fixed overhead before planning)
     extra = (args.nccl_allowance_mib << 20) if world > 1 else 0
+    if args.conv_math == "3xtf32":
+        # the 3xTF32 convolutions' low-part scratch is a fixed device allocation
+        _, d0 = trainer.export_network(args.arch, args.image, args.classes)
+        extra += trainer.precise_scratch_allowance(d0, args.image, args.cap_gib * (1 << 30))
     network_json, hardware_json, model_json, desc, plan_json, plan_s, prof_src = plan_for(args, extra)
     plan = json.loads(plan_json)
     k = plan["k_star"]

@@ -41,6 +41,14 @@ int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, const float*
  * 1 = 3xTF32 (hi/lo operand split, ~FP32 accuracy, 3x MMA work) */
 int accudnn_set_conv_math(int mode);
 int accudnn_get_conv_math(void);
+/* 3xTF32 on the TMA kernels: scratch for the operands' low parts
+ * (lo = v - tf32(v)) of the convolutions launched on `stream`; with it a
+ * precise convolution runs as three TF32 tcgen05 GEMMs (hi*hi + hi*lo +
+ * lo*hi accumulated into the output), without it on the cp.async kernel.
+ * ptr == NULL removes the entry.  accudnn_conv_precise_scratch_bytes: the
+ * bytes one convolution of shape d needs (max over fwd / dgrad / wgrad). */
+int accudnn_conv_set_precise_scratch(void* stream, void* ptr, unsigned long long bytes);
+unsigned long long accudnn_conv_precise_scratch_bytes(const accudnn_conv_desc* d);
 /* 1 = TMA-fed kernels where the shape allows (default), 0 = cp.async kernel only */
 int accudnn_set_conv_impl(int impl);
 /* split-K workspace of the persistent TMA kernels (deterministic fix-up:

@@ -121,6 +121,8 @@ CUDA_SYMBOLS = {
     "accudnn_get_conv_math": ([], _I),
     "accudnn_set_conv_impl": ([_I], _I),
     "accudnn_conv_set_workspace": ([ctypes.c_void_p, ctypes.c_ulonglong], _I),
+    "accudnn_conv_set_precise_scratch": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_ulonglong], _I),
+    "accudnn_conv_precise_scratch_bytes": ([_P], ctypes.c_ulonglong),
     "accudnn_conv_set_stream_workspace": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_ulonglong, _I], _I),
     "accudnn_conv_autotune": ([_I], _I),
     "accudnn_conv_tune_export": ([ctypes.POINTER(ctypes.c_void_p)], _I),

@@ -27,6 +27,9 @@
 // reduces with fp32 atomics for the small-M / huge-K weight gradients.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <vector>
+
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -518,6 +521,69 @@ int conv_tma_dgrad(const accudnn_conv_desc* d, const float* dy, const float* w, 
 int conv_tma_wgrad(const accudnn_conv_desc* d, const float* x, const float* dy, float* dw,
                    int beta, cudaStream_t st, int* rc);
 int g_conv_impl = 1;  // 1 = TMA kernels where eligible, 0 = cp.async kernel only
+
+// ---- 3xTF32 on the TMA kernels --------------------------------------------
+// The tensor core reads an fp32 operand as tf32 (its top 19 bits), so with
+// lo(v) = v - (v & 0xFFFFE000) materialised once per operand, three TF32
+// GEMMs accumulated into the output give hi*hi + hi*lo + lo*hi (~fp32
+// accuracy, as the cp.async PRECISE kernel computes per tile).  The lo copies
+// live in a caller-provided scratch per stream (accudnn_conv_set_precise_scratch);
+// without one the cp.async PRECISE kernel runs instead.
+__global__ void __launch_bounds__(256) tf32_lo_kernel(const float4* __restrict__ x,
+                                                      float4* __restrict__ lo, long long n4) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += gridDim.x * 256LL) {
+    const float4 v = __ldg(x + i);
+    float4 o;
+    o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    lo[i] = o;
+  }
+}
+
+struct Scratch {
+  cudaStream_t st;
+  char* ptr;
+  size_t bytes;
+};
+std::vector<Scratch> g_scratch;
+
+const Scratch* scratch_for(cudaStream_t st) {
+  for (const Scratch& e : g_scratch)
+    if (e.st == st) return &e;
+  return nullptr;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+
+int split_lo(const float* x, float* lo, long long n, cudaStream_t st) {
+  const long long n4 = n / 4;  // every conv operand has channels % 4 == 0
+  const int grid = static_cast<int>(std::min<long long>((n4 + 255) / 256, 8LL * sm_count()));
+  tf32_lo_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(x),
+                                       reinterpret_cast<float4*>(lo), n4);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// term(a, b, beta): one TF32 TMA GEMM of the mode (0 when the shape is not
+// TMA-eligible); out = a*b (+ old); returns 1 when handled, rc in *rc
+template <typename Term>
+int precise3(cudaStream_t st, const float* a, long long na, const float* b, long long nb,
+             int beta, int* rc, Term term) {
+  const Scratch* sc = scratch_for(st);
+  const size_t need = align256(sizeof(float) * na) + align256(sizeof(float) * nb);
+  if (!sc || sc->bytes < need) return 0;
+  float* a_lo = reinterpret_cast<float*>(sc->ptr);
+  float* b_lo = reinterpret_cast<float*>(sc->ptr + align256(sizeof(float) * na));
+  if (!term(a, b, beta, rc)) return 0;  // hi * hi (not eligible: nothing written)
+  if (*rc) return 1;
+  if ((*rc = split_lo(a, a_lo, na, st)) != 0) return 1;
+  if ((*rc = split_lo(b, b_lo, nb, st)) != 0) return 1;
+  term(a, b_lo, 1, rc);  // + hi * lo
+  if (*rc) return 1;
+  term(a_lo, b, 1, rc);  // + lo * hi
+  return 1;
+}
 }  // namespace accudnn
 
 using namespace accudnn;
@@ -529,6 +595,12 @@ extern "C" int accudnn_conv_fwd(const accudnn_conv_desc* d, const float* x, cons
   if (!valid_desc(d)) return static_cast<int>(cudaErrorInvalidValue);
   int rc = 0;
   if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_fwd(d, x, w, y, beta, stream, &rc))
+    return rc;
+  if (g_conv_impl == 1 && g_conv_math == 1 &&
+      precise3(stream, x, 1LL * d->n * d->h * d->w * d->c, w, 1LL * d->k * d->r * d->s * d->c, beta,
+               &rc, [&](const float* xa, const float* wb, int bt, int* r) {
+                 return conv_tma_fwd(d, xa, wb, y, bt, stream, r);
+               }))
     return rc;
   Args a = make_args(d, FWD);
   a.a_src = x; a.b_src = w; a.out = y; a.beta = beta;
@@ -560,6 +632,12 @@ extern "C" int accudnn_conv_dgrad(const accudnn_conv_desc* d, const float* dy, c
   int rc = 0;
   if (g_conv_impl == 1 && g_conv_math == 0 && conv_tma_dgrad(d, dy, w, dx, beta, stream, &rc))
     return rc;
+  if (g_conv_impl == 1 && g_conv_math == 1 &&
+      precise3(stream, dy, 1LL * d->n * d->p * d->q * d->k, w, 1LL * d->k * d->r * d->s * d->c, beta,
+               &rc, [&](const float* ya, const float* wb, int bt, int* r) {
+                 return conv_tma_dgrad(d, ya, wb, dx, bt, stream, r);
+               }))
+    return rc;
   Args a = make_args(d, DGRAD);
   a.a_src = dy; a.b_src = w; a.out = dx; a.beta = beta;
   return dispatch<DGRAD>(a, 1, stream);
@@ -574,6 +652,12 @@ extern "C" int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, co
   if (g_conv_impl == 1 && g_conv_math == 0 && splits <= 0 &&
       conv_tma_wgrad(d, x, dy, dw, beta, stream, &rc))
     return rc;
+  if (g_conv_impl == 1 && g_conv_math == 1 && splits <= 0 &&
+      precise3(stream, x, 1LL * d->n * d->h * d->w * d->c, dy, 1LL * d->n * d->p * d->q * d->k, beta,
+               &rc, [&](const float* xa, const float* yb, int bt, int* r) {
+                 return conv_tma_wgrad(d, xa, yb, dw, bt, stream, r);
+               }))
+    return rc;
   Args a = make_args(d, WGRAD);
   a.a_src = dy; a.b_src = x; a.out = dw; a.beta = beta;
   if (splits <= 0) splits = pick_splits(a, sm_count());
@@ -584,6 +668,27 @@ extern "C" int accudnn_conv_wgrad(const accudnn_conv_desc* d, const float* x, co
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   return dispatch<WGRAD>(a, splits, stream);
+}
+
+extern "C" int accudnn_conv_set_precise_scratch(void* stream, void* ptr, unsigned long long bytes) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (size_t i = 0; i < accudnn::g_scratch.size(); ++i)
+    if (accudnn::g_scratch[i].st == st) {
+      accudnn::g_scratch.erase(accudnn::g_scratch.begin() + static_cast<long>(i));
+      break;
+    }
+  if (ptr && bytes)
+    accudnn::g_scratch.push_back({st, static_cast<char*>(ptr), static_cast<size_t>(bytes)});
+  return 0;
+}
+
+extern "C" unsigned long long accudnn_conv_precise_scratch_bytes(const accudnn_conv_desc* d) {
+  using accudnn::align256;
+  if (!d) return 0;
+  const size_t x = align256(sizeof(float) * d->n * d->h * d->w * d->c);
+  const size_t y = align256(sizeof(float) * d->n * d->p * d->q * d->k);
+  const size_t w = align256(sizeof(float) * d->k * d->r * d->s * d->c);
+  return std::max({x + w, y + w, x + y});
 }
 
 extern "C" int accudnn_set_conv_math(int mode) {

@@ -62,6 +62,8 @@ struct Executor::Impl {
   cudaStream_t input_stream = nullptr;  // pipelined next-batch H2D
   cudaStream_t side = nullptr;          // concurrent weight gradients
   void* side_ws = nullptr;              // its split-K workspace
+  void* precise_scratch = nullptr;      // 3xTF32: operand low parts (compute stream)
+  size_t precise_bytes = 0;
   std::vector<cudaEvent_t> fork_ev;     // per step: dy ready on the compute stream
   std::vector<cudaEvent_t> wg_done;     // per step: that step's weight gradient done
   std::vector<int> side_last;           // per instance: last step whose wgrad reads it
@@ -136,6 +138,29 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
     if (!cfg.conv_bn_stats) need = 0;
     I.bn_stats_bytes = need;
     fixed_bytes_ += 2 * need;
+  }
+  // 3xTF32 (fp32-accurate) convolutions on the TMA kernels: scratch for the
+  // operands' low parts, sized for the largest convolution of the net at k;
+  // the weight-gradient side stream is not used in this mode (one scratch)
+  const bool precise = accudnn_get_conv_math() == 1;
+  size_t precise_bytes = 0;
+  if (precise) {
+    for (int o = 0; o < n; ++o) {
+      const Op& op = net_.ops[static_cast<size_t>(o)];
+      if (op.kind != OpKind::conv && op.kind != OpKind::fc) continue;
+      accudnn_conv_desc d{};
+      if (op.kind == OpKind::fc) {
+        d = accudnn_conv_desc{static_cast<int>(k), 1, 1, op.cin, op.cout, 1, 1, 1, 0, 1, 1};
+      } else {
+        const int ih = op.in0 == kImage ? net_.image : net_.shape[static_cast<size_t>(op.in0)].h;
+        const int iw = op.in0 == kImage ? net_.image : net_.shape[static_cast<size_t>(op.in0)].w;
+        const TensorShape& so = net_.shape[static_cast<size_t>(o)];
+        d = accudnn_conv_desc{static_cast<int>(k), ih, iw, op.cin, op.cout, op.r, op.s,
+                              op.stride, op.pad, so.h, so.w};
+      }
+      precise_bytes = std::max<size_t>(precise_bytes, accudnn_conv_precise_scratch_bytes(&d));
+    }
+    fixed_bytes_ += precise_bytes;
   }
   // split-K workspace of the convolutions: whatever the planner's fixed
   // allowance leaves, capped at 64 MiB; the kernels pick their split
@@ -250,6 +275,8 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ck(cudaMalloc(&I.loss, 256), "loss");
   ck(cudaMallocHost(&I.loss_host, sizeof(float)), "loss host");
   if (conv_ws) ck(cudaMalloc(&I.conv_ws, conv_ws), "conv workspace");
+  I.precise_bytes = precise_bytes;
+  if (precise_bytes) ck(cudaMalloc(&I.precise_scratch, precise_bytes), "3xTF32 scratch");
   if (side_ws) ck(cudaMalloc(&I.side_ws, side_ws), "side conv workspace");
   if (I.bn_stats_bytes)
     for (auto& p : I.bn_stats) ck(cudaMalloc(&p, I.bn_stats_bytes), "bn stats");
@@ -310,6 +337,9 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   ckl(accudnn_conv_set_stream_workspace(I.compute, I.conv_ws, I.conv_ws ? conv_ws : 0,
                                         I.conv_ws ? 0 : -1),
       "compute workspace");
+  if (I.precise_scratch)
+    ckl(accudnn_conv_set_precise_scratch(I.compute, I.precise_scratch, I.precise_bytes),
+        "precise scratch");
   ckl(accudnn_conv_set_stream_workspace(I.side, I.side_ws, I.side_ws ? side_ws : 0,
                                         cfg.side_ctas > 0 ? cfg.side_ctas : (I.side_ws ? 0 : -1)),
       "side workspace");
@@ -374,6 +404,10 @@ Executor::~Executor() {
   if (I.graph) cudaGraphExecDestroy(I.graph);
   if (I.comm) ncclCommDestroy(I.comm);
   if (I.side) accudnn_conv_set_stream_workspace(I.side, nullptr, 0, 0);
+  if (I.precise_scratch) {
+    accudnn_conv_set_precise_scratch(I.compute, nullptr, 0);
+    cudaFree(I.precise_scratch);
+  }
   if (I.compute) accudnn_conv_set_stream_workspace(I.compute, nullptr, 0, 0);
   for (auto* v : {&I.step_done, &I.d2h_done, &I.h2d_done, &I.phase_begin, &I.phase_end,
                   &I.bucket_ready, &I.fork_ev, &I.wg_done, &I.ar_begin, &I.ar_end, &I.out_b, &I.out_e, &I.in_b, &I.in_e})
@@ -460,7 +494,9 @@ StepStats Executor::step(const void* images, const int* labels, int host_inputs,
   cudaStream_t cs = I.compute;
   void* csv = static_cast<void*>(cs);
   StepStats st;
-  const bool use_side = cfg_.wgrad_stream && !profile && !I.first_step;
+  // (3xTF32: the weight gradients stay on the compute stream, which owns the
+  // precise scratch)
+  const bool use_side = cfg_.wgrad_stream && !profile && !I.first_step && !I.precise_scratch;
   int last_wg = 0;  // latest step with a side-stream weight gradient
 
   auto act = [&](int t, int step) -> float* {

@@ -88,6 +88,33 @@ def default_m_others(describe, image, budget_bytes=None):
     return momentum + stats + staging
 
 
+def precise_scratch_allowance(describe, image, budget_bytes):
+    """Fixed device bytes of the 3xTF32 mode (accudnn_set_conv_math(1)): the
+    executor's scratch for the operands' low parts of its largest
+    convolution (max over fwd / dgrad / wgrad of the two operands' bytes,
+    accudnn_conv_precise_scratch_bytes), at the largest batch the budget
+    could hold at all (as default_m_others sizes the input staging)."""
+    ops = describe["ops"]
+    fm_per_image = sum(4 * o["out"][0] * o["out"][1] * o["out"][2] for o in ops
+                       if not o.get("transient"))
+    k_ub = max(1, int(budget_bytes) // max(1, fm_per_image))
+    by_id = {o["id"]: o for o in ops}
+    worst = 0
+    for o in ops:
+        if o["kind"] not in ("conv", "fc"):
+            continue
+        src = by_id.get(o["in0"])
+        xin = (image * image * o["cin"]) if src is None else \
+            src["out"][0] * src["out"][1] * src["out"][2]
+        if o["kind"] == "fc":
+            xin = o["cin"]
+        yout = o["out"][0] * o["out"][1] * o["out"][2] if o["kind"] == "conv" else o["cout"]
+        w = o["cout"] * o["cin"] * o.get("r", 1) ** 2
+        x, y = 4 * xin * k_ub, 4 * yout * k_ub
+        worst = max(worst, x + 4 * w, y + 4 * w, x + y)
+    return worst + (4 << 20)  # 256-byte alignment of the two parts and slack
+
+
 def config_documents(arch, image, classes, cap_bytes, k_base=8):
     """The planner's input documents for one BASELINE configuration, exactly
     as bench.py and the headline plan goldens build them: network.json from
