@@ -142,7 +142,9 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
   // 3xTF32 (fp32-accurate) convolutions on the TMA kernels: scratch for the
   // operands' low parts, sized for the largest convolution of the net at k;
   // the weight-gradient side stream is not used in this mode (one scratch)
-  const bool precise = accudnn_get_conv_math() == 1;
+  // (ACCUDNN_PRECISE_TMA=0: the cp.async PRECISE kernel instead, for A/B checks)
+  const char* ptma = std::getenv("ACCUDNN_PRECISE_TMA");
+  const bool precise = accudnn_get_conv_math() == 1 && !(ptma && std::atoi(ptma) == 0);
   size_t precise_bytes = 0;
   if (precise) {
     for (int o = 0; o < n; ++o) {
