@@ -1761,7 +1761,9 @@ int run_call(const Call& c, cudaStream_t st) {
     }
   }
   int r = launch_cfg(c, cfg, st);
-  if (r == -1 && cfg.sk) r = launch_cfg(c, model_cfg(c), st);  // e.g. a smaller workspace now
+  // a tuned stream-K or K-split-pair entry that this call cannot use (a smaller
+  // workspace now, BN statistics requested): the analytic config instead
+  if (r == -1 && (cfg.sk || cfg.cm == 5)) r = launch_cfg(c, model_cfg(c), st);
   return r;
 }
 
