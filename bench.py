@@ -580,9 +580,10 @@ def run_ours(args):
             "their kernels (TMA/tcgen05 conv, cp.async conv, split-K reduce) in the profiled "
             "serial step; achieved_phase_events = same FLOPs / CUDA-event phase times")
     # DRAM traffic of the conv kernels per launch, from the committed ncu
-    # launch list of the same step (profiles/r01, dram__bytes_read+write)
-    ls_path = os.path.join(ROOT, "profiles", "r01", f"launch_summary_k{k}.json")
-    if os.path.exists(ls_path):
+    # launch list of the same step (latest round first, dram__bytes_read+write)
+    ls_path = next((p for p in (os.path.join(ROOT, "profiles", r, f"launch_summary_k{k}.json")
+                                for r in ("r02", "r01")) if os.path.exists(p)), "")
+    if ls_path:
         summ = json.load(open(ls_path))
         cv = [v for n, v in summ.items() if "conv_sm100_kernel" in n or "conv_igemm_kernel" in n]
         n_launch = sum(v["launches"] for v in cv)
