@@ -1207,6 +1207,136 @@ extern "C" int accudnn_bn_fwd(const float* x, long long M, int C, const float* g
 
 // forward batch norm whose statistics come from the producing convolution
 // (accudnn_conv_fwd_stats): only the normalise pass reads x
+namespace accudnn {
+namespace {
+// ---- batch norm forward from the producing conv's statistics ----------------
+// With the column sums / sums of squares of every 32-row slot of x written by
+// the conv epilogue ([2][P][C], accudnn_conv_fwd_stats), the forward needs no
+// statistics pass over x and no grid-wide exchange: a small kernel finalises
+// the per-channel scale / shift (fixed-order reduction, so every element sees
+// the same coefficients) and an element-wise kernel normalises.
+__global__ void __launch_bounds__(256) bn_stats_finalize_kernel(
+    const float* __restrict__ stats, long long P, int C, long long M, const float* gamma,
+    const float* beta, float eps, float momentum, float* run_mean, float* run_var,
+    float* save_mean, float* save_invstd, float* __restrict__ coef) {
+  __shared__ double red[2][256][4];
+  const int c = blockIdx.x * 4;
+  double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+#pragma unroll 4
+  for (long long r = threadIdx.x; r < P; r += 256) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(stats + r * C + c));
+    const float4 q = __ldcg(reinterpret_cast<const float4*>(stats + (P + r) * C + c));
+    s1[0] += v.x; s1[1] += v.y; s1[2] += v.z; s1[3] += v.w;
+    s2[0] += q.x; s2[1] += q.y; s2[2] += q.z; s2[3] += q.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    red[0][threadIdx.x][j] = s1[j];
+    red[1][threadIdx.x][j] = s2[j];
+  }
+  __syncthreads();
+  for (int n = 128; n >= 1; n >>= 1) {  // fixed-shape tree
+    if (static_cast<int>(threadIdx.x) < n)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        red[0][threadIdx.x][j] += red[0][threadIdx.x + n][j];
+        red[1][threadIdx.x][j] += red[1][threadIdx.x + n][j];
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) {
+    const int j = threadIdx.x, ch = c + j;
+    const double mean = red[0][0][j] / static_cast<double>(M);
+    double var = red[1][0][j] / static_cast<double>(M) - mean * mean;
+    if (var < 0) var = 0;
+    const float inv = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+    const float sc = gamma[ch] * inv;
+    coef[ch] = sc;
+    coef[C + ch] = beta[ch] - static_cast<float>(mean) * sc;
+    if (save_mean) save_mean[ch] = static_cast<float>(mean);
+    if (save_invstd) save_invstd[ch] = inv;
+    if (run_mean && run_var && M > 1) {
+      const double unbiased = var * static_cast<double>(M) / static_cast<double>(M - 1);
+      run_mean[ch] = (1.f - momentum) * run_mean[ch] + momentum * static_cast<float>(mean);
+      run_var[ch] = (1.f - momentum) * run_var[ch] + momentum * static_cast<float>(unbiased);
+    }
+  }
+}
+
+template <bool RELU, bool SKIP>
+__global__ void __launch_bounds__(256) bn_apply_kernel(const float4* __restrict__ x,
+                                                       const float4* __restrict__ skip,
+                                                       const float* __restrict__ coef, int C,
+                                                       long long n4, float4* __restrict__ y) {
+  const int c4 = C >> 2;
+  const float4* sc4 = reinterpret_cast<const float4*>(coef);
+  const float4* sh4 = reinterpret_cast<const float4*>(coef + C);
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += gridDim.x * 256LL) {
+    const int q = static_cast<int>(i % c4);
+    const float4 sc = __ldg(sc4 + q), sh = __ldg(sh4 + q);
+    float4 v = __ldcs(x + i);
+    v.x = v.x * sc.x + sh.x;
+    v.y = v.y * sc.y + sh.y;
+    v.z = v.z * sc.z + sh.z;
+    v.w = v.w * sc.w + sh.w;
+    if (SKIP) {
+      const float4 k = __ldcs(skip + i);
+      v.x += k.x;
+      v.y += k.y;
+      v.z += k.z;
+      v.w += k.w;
+    }
+    if (RELU) {
+      v.x = fmaxf(v.x, 0.f);
+      v.y = fmaxf(v.y, 0.f);
+      v.z = fmaxf(v.z, 0.f);
+      v.w = fmaxf(v.w, 0.f);
+    }
+    y[i] = v;
+  }
+}
+
+// ACCUDNN_BN_STATS_SPLIT=0: the cooperative fused kernel with stats_in instead
+bool bn_stats_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ACCUDNN_BN_STATS_SPLIT");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+int bn_fwd_from_stats(const float* x, const float* stats, const float* skip, long long M, int C,
+                      const float* gamma, const float* beta, float eps, int relu, float* y,
+                      float* save_mean, float* save_invstd, float* running_mean,
+                      float* running_var, float momentum, void* ws, cudaStream_t st) {
+  // coefficients in the BN workspace's partial area (2 C floats)
+  float* coef = bn_ws(ws, C).part;
+  const long long P = (M + 31) / 32;
+  bn_stats_finalize_kernel<<<C / 4, 256, 0, st>>>(stats, P, C, M, gamma, beta, eps, momentum,
+                                                  running_mean, running_var, save_mean,
+                                                  save_invstd, coef);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return static_cast<int>(e);
+  const long long n4 = M * C / 4;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = static_cast<int>(std::min<long long>((n4 + 255) / 256, 8LL * sms));
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* k4 = reinterpret_cast<const float4*>(skip);
+  float4* y4 = reinterpret_cast<float4*>(y);
+  if (skip)
+    bn_apply_kernel<true, true><<<grid, 256, 0, st>>>(x4, k4, coef, C, n4, y4);
+  else if (relu)
+    bn_apply_kernel<true, false><<<grid, 256, 0, st>>>(x4, k4, coef, C, n4, y4);
+  else
+    bn_apply_kernel<false, false><<<grid, 256, 0, st>>>(x4, k4, coef, C, n4, y4);
+  return static_cast<int>(cudaGetLastError());
+}
+}  // namespace
+}  // namespace accudnn
+
 extern "C" int accudnn_bn_fwd_stats(const float* x, const float* stats, long long M, int C,
                                     const float* gamma, const float* beta, float eps, int relu,
                                     float* y, float* save_mean, float* save_invstd,
@@ -1214,6 +1344,9 @@ extern "C" int accudnn_bn_fwd_stats(const float* x, const float* stats, long lon
                                     void* ws, void* stream) {
   if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups || !stats)
     return static_cast<int>(cudaErrorInvalidValue);
+  if (bn_stats_split())
+    return bn_fwd_from_stats(x, stats, nullptr, M, C, gamma, beta, eps, relu, y, save_mean,
+                             save_invstd, running_mean, running_var, momentum, ws, S(stream));
   BnArgs a{};
   a.x = x;
   a.stats_in = stats;
@@ -1292,6 +1425,9 @@ extern "C" int accudnn_bn_add_relu_fwd_stats(const float* x, const float* stats,
                                              float momentum, void* ws, void* stream) {
   if ((C & 3) || M <= 0 || C > 32 * kBnMaxGroups || !stats)
     return static_cast<int>(cudaErrorInvalidValue);
+  if (bn_stats_split())
+    return bn_fwd_from_stats(x, stats, skip, M, C, gamma, beta, eps, 1, y, save_mean, save_invstd,
+                             running_mean, running_var, momentum, ws, S(stream));
   BnArgs a{};
   a.x = x;
   a.stats_in = stats;
