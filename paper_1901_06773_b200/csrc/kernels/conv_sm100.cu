@@ -1078,6 +1078,62 @@ __global__ void __launch_bounds__(256) conv_splitk_reduce_kernel(const Prob a) {
 // the output.  Block = 32 rows x 32 columns (thread = row x float4): slices
 // summed in order per element, then the column sums over the 32 rows in a
 // fixed smem order -> one [2][P][Ng] partial slot per (32-row block, column).
+// Many slices (the weight gradients' long-K GEMMs: 16-128 slices of a small
+// output): a group of 8 lanes per output float4, lane g summing slices
+// g, g+8, ... in order (all loads of a lane in flight at once), then a fixed
+// xor-shuffle tree over the group -- one memory round trip instead of
+// splits/8 sequential ones, and still the same order on every run.
+__global__ void __launch_bounds__(256) conv_splitk_reduce_wide_kernel(const Prob a) {
+  pdl_wait();
+  pdl_trigger();
+  const int ng4 = a.Ng >> 2;
+  const long long total = static_cast<long long>(a.M) * ng4;
+  const long long slice = static_cast<long long>(a.M) * a.Ng;
+  const int g = threadIdx.x & 7;
+  for (long long i = (blockIdx.x * 256LL + threadIdx.x) >> 3; i < total;
+       i += static_cast<long long>(gridDim.x) * 32) {
+    const int m = static_cast<int>(i / ng4);
+    const int c = static_cast<int>(i - static_cast<long long>(m) * ng4) * 4;
+    const float* src = a.ws + static_cast<long long>(m) * a.Ng + c;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = g; s0 < a.splits; s0 += 64) {
+      float4 p[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + 8 * u < a.splits)
+          p[u] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + 8 * u) * slice));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + 8 * u < a.splits) {
+          o.x += p[u].x;
+          o.y += p[u].y;
+          o.z += p[u].z;
+          o.w += p[u].w;
+        }
+    }
+    // the 8 lanes of this group (groups of a warp may leave the loop apart)
+    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1) {
+      o.x += __shfl_xor_sync(gmask, o.x, off, 8);
+      o.y += __shfl_xor_sync(gmask, o.y, off, 8);
+      o.z += __shfl_xor_sync(gmask, o.z, off, 8);
+      o.w += __shfl_xor_sync(gmask, o.w, off, 8);
+    }
+    if (g == 0) {
+      float4* d = reinterpret_cast<float4*>(a.out + out_row(a, m) + c);
+      if (a.beta) {
+        const float4 old = *d;
+        o.x += old.x;
+        o.y += old.y;
+        o.z += old.z;
+        o.w += old.w;
+      }
+      *d = o;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) conv_splitk_reduce_stats_kernel(const Prob a) {
   pdl_wait();
   pdl_trigger();
@@ -1328,6 +1384,11 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
     return static_cast<int>(cudaGetLastError());
   }
   const long long vec = static_cast<long long>(a.M) * (a.Ng / 4);
+  if (a.splits >= 16) {  // 8 lanes per output vector
+    const int wgrid = static_cast<int>(std::min<long long>((vec * 8 + 255) / 256, 16LL * sm_count()));
+    launch_pdl(conv_splitk_reduce_wide_kernel, wgrid, 256, 0, st, a);
+    return static_cast<int>(cudaGetLastError());
+  }
   const int rgrid = static_cast<int>(std::min<long long>((vec + 255) / 256, 8LL * sm_count()));
   launch_pdl(conv_splitk_reduce_kernel, rgrid, 256, 0, st, a);
   return static_cast<int>(cudaGetLastError());

@@ -73,6 +73,7 @@ struct BnArgs {
   const float* dy;
   long long M;
   int C, lanes, Y, relu;
+  long long rpb;  // rows per block (0: ceil(M / Y))
   const float* gamma;
   const float* beta;
   const float* mean;     // mode 1
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   const bool lane_ok = lane_r < rows_per_pass;
   const int c = (blockIdx.x * lanes + lane_c) * 4;
   const bool c_ok = lane_ok && c < a.C;
-  const long long rows_per_block = (a.M + a.Y - 1) / a.Y;
+  const long long rows_per_block = a.rpb > 0 ? a.rpb : (a.M + a.Y - 1) / a.Y;
   const long long r_begin = blockIdx.y * rows_per_block;
   const long long r_end = min(a.M, r_begin + rows_per_block);
   const long long C = a.C;
@@ -650,6 +651,16 @@ __device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c
 //  * cooperative: Y row splits over the whole grid (all CTAs co-resident,
 //    2 per SM), partials in the workspace, one grid barrier; for the large
 //    early-stage layers that need every SM streaming.
+// ACCUDNN_BN_RPB=0: plain ceil(M / Y) row splits (A/B switch)
+inline bool rpb_rounding() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ACCUDNN_BN_RPB");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 template <int MODE, bool SKIP>
 int bn_launch(BnArgs a, cudaStream_t st) {
   // L2 eviction priorities (ACCUDNN_BN_L2HINTS: 0 off, 1 auto, 3 always,
@@ -740,6 +751,20 @@ int bn_launch(BnArgs a, cudaStream_t st) {
   y = std::min<long long>(y, 16LL * T);
   y = std::min<long long>(y, max_blocks / gx);
   if (y < 1) y = 1;
+  // rows per block a multiple of 4 x the rows one pass of the block covers:
+  // every thread then streams whole batches of 4 rows (a ragged remainder is
+  // one dependent round trip per row -- 3 of them on a 14x14 layer)
+  {
+    const long long rpp = kBnThreads / l;
+    const long long unit = 4 * rpp;
+    long long rpb = (a.M + y - 1) / y;
+    rpb = (rpb + unit - 1) / unit * unit;
+    const long long y2 = (a.M + rpb - 1) / rpb;
+    if (rpb_rounding() && y2 >= 1 && y2 <= y) {
+      y = y2;
+      a.rpb = rpb;
+    }
+  }
   a.Y = static_cast<int>(y);
   cfg.gridDim = dim3(gx, a.Y);
   attr[0].id = cudaLaunchAttributeCooperative;
