@@ -754,13 +754,22 @@ int bn_launch(BnArgs a, cudaStream_t st) {
   // rows per block a multiple of 4 x the rows one pass of the block covers:
   // every thread then streams whole batches of 4 rows (a ragged remainder is
   // one dependent round trip per row -- 3 of them on a 14x14 layer)
+  // Taken when it saves at least two dependent round trips per thread (a
+  // layer whose threads own 3-4 rows: 3 -> 1), not when it only trades one
+  // for fewer CTAs streaming a large layer (measured per shape, bn_bench)
   {
     const long long rpp = kBnThreads / l;
     const long long unit = 4 * rpp;
-    long long rpb = (a.M + y - 1) / y;
-    rpb = (rpb + unit - 1) / unit * unit;
+    auto rounds = [&](long long rpb) {  // worst thread: batches of 4 + single rows
+      long long worst = 0;
+      for (long long rpt : {rpb / rpp, (rpb + rpp - 1) / rpp})
+        worst = std::max(worst, rpt / 4 + rpt % 4);
+      return worst;
+    };
+    const long long rpb0 = (a.M + y - 1) / y;
+    const long long rpb = (rpb0 + unit - 1) / unit * unit;
     const long long y2 = (a.M + rpb - 1) / rpb;
-    if (rpb_rounding() && y2 >= 1 && y2 <= y) {
+    if (rpb_rounding() && y2 >= 1 && y2 <= y && rounds(rpb0) - rounds(rpb) >= 2) {
       y = y2;
       a.rpb = rpb;
     }
