@@ -93,6 +93,11 @@ struct Prob {
   // [c*T/G, (c+1)*T/G) of the tile-major iteration space T = tiles * kb_total;
   // a tile cut between CTAs leaves one partial per segment in its workspace
   // block and the last-arriving segment sums them in segment order
+  // 2-slice split-K reduced in L2: the output is zeroed first and both
+  // slices bulk reduce-add their tiles into it; (0 + a) + b == (0 + b) + a
+  // bit for bit (one rounding per add, the first exact), so the arrival
+  // order does not matter -- no workspace, no reduce kernel
+  int pair_add;
   int streamk;
   int sk_maxseg;       // segments per tile at most (workspace blocks per tile)
   unsigned* fix_cnt;   // per-tile arrival counters (zero between launches)
@@ -726,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t trow = tmem + static_cast<uint32_t>(acc * BN) +
                             (static_cast<uint32_t>(quad * 32) << 16);
       const int ncols = min(BN, a.Ng - n0);  // multiple of 4
-      const bool partial = nseg > 1 && !KC;
+      const bool partial = nseg > 1 && !KC && !a.pair_add;
       // stream-K partial: plain stores into the segment's workspace block
       // [128][BN] (the tile's other segments may still be running)
       const bool skp = kSK && a.streamk && partial;
@@ -855,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             if (partial)
               tma_store_3d(&tmC, sbuf, n0 + c0, m0, split);
-            else if (a.beta)
+            else if (a.beta || a.pair_add)
               tma_reduce_add_2d(&tmC, sbuf, n0 + c0, m0);
             else
               tma_store_2d(&tmC, sbuf, n0 + c0, m0);
@@ -1376,7 +1381,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   cudaError_t e =
       cudaLaunchKernelEx(&cfg, conv_sm100_kernel<MODE, BN, STAGES, CM, BS, G, SK, KC>, ta, tb, tc, a);
   if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess || a.splits == 1 || KC) return static_cast<int>(e);
+  if (e != cudaSuccess || a.splits == 1 || KC || a.pair_add) return static_cast<int>(e);
   if (a.stats) {
     const long long blocks = (static_cast<long long>(a.M) + 31) / 32 * (a.Ng / 32);
     const int rgrid = static_cast<int>(std::min<long long>(blocks, 16LL * sm_count()));
@@ -1592,6 +1597,14 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
     if (c.mode == WGRAD || cfg.splits != 2 || cfg.bs || cfg.sk || a.scatter || a.stats) return -1;
     cfg.cm = 1;
   }
+  // cm 6: 2-slice split-K reduced by bulk reduce-adds into the zeroed output
+  // (overwrite calls with row-major outputs only: with beta = 1 the old value
+  // would make the order matter)
+  const bool padd = cfg.cm == 6;
+  if (padd) {
+    if (cfg.splits != 2 || cfg.bs || cfg.sk || a.scatter || a.stats || a.beta) return -1;
+    cfg.cm = 1;
+  }
   if (c.mode == WGRAD) cfg.cm = 1;  // multicast of B across M-tiles: FWD / DGRAD only
   if (cfg.bs && (c.mode == WGRAD || cfg.splits != 1 || cfg.cm != 1 ||
                  static_cast<size_t>(c.a.kb_total) * cfg.bn * kBK * 4 > kMaxBStat))
@@ -1638,7 +1651,8 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   CUtensorMap tc;
   std::memset(&tc, 0, sizeof(tc));
   a.tma_out = 0;
-  if (a.splits > 1 && !kc) {
+  a.pair_add = padd ? 1 : 0;
+  if (a.splits > 1 && !kc && !padd) {
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.Ng), static_cast<cuuint64_t>(a.M),
                                 static_cast<cuuint64_t>(a.splits)};
     const cuuint64_t str[2] = {static_cast<cuuint64_t>(a.Ng) * 4,
@@ -1652,6 +1666,12 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
     a.tma_out = tiled_map(&tc, a.out, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
   }
   if (cfg.bs && a.tiles_n > sm_count()) cfg.bs = 0;
+  if (padd) {
+    if (!a.tma_out) return -1;
+    const cudaError_t e =
+        cudaMemsetAsync(a.out, 0, sizeof(float) * static_cast<size_t>(a.M) * a.Ng, st);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
   if (kc) {
     if (!a.tma_out) return -1;
     return c.mode == FWD ? dispatch_kc<FWD>(ta, tb, tc, a, cfg.bn, st)
@@ -1706,8 +1726,8 @@ Cfg tune(const Call& c, cudaStream_t st) {
   // 0: plain, 1: 2-CTA multicast, 3: 2-SM MMA pair.  (2, B-stationary, is
   // available through accudnn_conv_force_cfg but not tuned: measured no faster)
   // 5: split-K over a DSMEM-reduced CTA pair (2 slices)
-  for (int variant : {0, 1, 3, 5}) {
-   const int cm = variant == 1 ? 2 : variant == 3 ? 4 : variant == 5 ? 5 : 1;
+  for (int variant : {0, 1, 3, 5, 6}) {
+   const int cm = variant == 1 ? 2 : variant == 3 ? 4 : variant >= 5 ? variant : 1;
    const int bs = variant == 2 ? 1 : 0;
    if (variant > 0 && c.mode == WGRAD) continue;
    for (int bn : {64, 128, 256}) {
@@ -1717,7 +1737,7 @@ Cfg tune(const Call& c, cudaStream_t st) {
      // s = 0: stream-K (single-CTA tiles only)
      for (int sk : {0, 1}) {
       if (sk && (s != 1 || cm != 1 || bs)) continue;
-      if (cm == 5 && (s != 2 || sk)) continue;
+      if (cm >= 5 && (s != 2 || sk)) continue;
       if (!splits_ok(c, s)) continue;
       if (bs && s != 1) continue;
       const Cfg cand{bn, s, cm, bs, sk};
@@ -1775,6 +1795,14 @@ int run_call(const Call& c, cudaStream_t st) {
       f.bs = 1;
       f.splits = 1;
     }
+    if (g_force.cm == 6) {  // test hook: 2-slice split-K by reduce-adds into the zeroed output
+      f.splits = 2;
+      f.bs = 0;
+      f.sk = 0;
+      const int r = launch_cfg(c, f, st);
+      if (r != -1) return r;
+      f = model_cfg(c);
+    }
     if (g_force.cm == 5) {  // test hook: split-K pair reduced through DSMEM
       f.splits = 2;
       f.bs = 0;
@@ -1824,7 +1852,7 @@ int run_call(const Call& c, cudaStream_t st) {
   int r = launch_cfg(c, cfg, st);
   // a tuned stream-K or K-split-pair entry that this call cannot use (a smaller
   // workspace now, BN statistics requested): the analytic config instead
-  if (r == -1 && (cfg.sk || cfg.cm == 5)) r = launch_cfg(c, model_cfg(c), st);
+  if (r == -1 && (cfg.sk || cfg.cm >= 5)) r = launch_cfg(c, model_cfg(c), st);
   return r;
 }
 
@@ -2076,7 +2104,8 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     for (int& v : key) ok = ok && static_cast<bool>(ls >> v);
     ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
     if (!ok) continue;
-    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4 && cfg.cm != 5)) cfg.cm = 1;
+    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4 && cfg.cm != 5 && cfg.cm != 6))
+      cfg.cm = 1;
     if (!(ls >> cfg.bs) || (cfg.bs != 0 && cfg.bs != 1)) cfg.bs = 0;
     if (!(ls >> cfg.sk) || (cfg.sk != 0 && cfg.sk != 1)) cfg.sk = 0;
     if (cfg.bn != 64 && cfg.bn != 128 && cfg.bn != 256) continue;

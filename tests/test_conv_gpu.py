@@ -65,7 +65,8 @@ def check(got, ref):
 
 @pytest.fixture(params=["tma", "tma_cluster2", "tma_pair", "tma_pair_bn256_split2", "tma_pair_bn64",
                         "tma_bn64_split3", "tma_bstat", "tma_streamk", "tma_streamk_bn64",
-                        "tma_kpair", "tma_kpair_bn256", "tma_kpair_bn64", "cpasync"])
+                        "tma_kpair", "tma_kpair_bn256", "tma_kpair_bn64", "tma_padd", "tma_padd_bn256",
+                        "cpasync"])
 def impl(request):
     """TMA kernel with the analytic config, with the B tile multicast across an
     M-tile pair (cluster of 2), as a CTA pair running 2-SM MMAs (256-row
@@ -95,6 +96,10 @@ def impl(request):
         lib.accudnn_conv_force_cfg(256, 0, 5)
     elif request.param == "tma_kpair_bn64":
         lib.accudnn_conv_force_cfg(64, 0, 5)
+    elif request.param == "tma_padd":  # 2 slices reduce-added into the zeroed output
+        lib.accudnn_conv_force_cfg(0, 0, 6)
+    elif request.param == "tma_padd_bn256":
+        lib.accudnn_conv_force_cfg(256, 0, 6)
     yield request.param
     lib.accudnn_conv_force_cfg(0, 0, 0)
     lib.accudnn_set_conv_impl(1)
@@ -372,6 +377,15 @@ def test_kpair_equals_two_slice_workspace_reduction(cuda_dev, shape, bn):
     for u, v, t in zip(ws, kp, again):
         assert torch.equal(u, v)
         assert torch.equal(v, t)
+    # cm 6: the same two slices reduce-added into the zeroed output in L2
+    # (overwrite calls; accumulating calls fall back to another config)
+    pa = run(6)
+    pa2 = run(6)
+    for i in (0, 2):  # y, dx (beta = 0)
+        assert torch.equal(ws[i], pa[i])
+        assert torch.equal(pa[i], pa2[i])
+    for i in (1, 3):
+        assert rel_err(pa[i].double(), ws[i].double()) < 1e-6
     ref = F.conv2d(x_d.permute(0, 3, 1, 2).double().cpu(), w_d.permute(0, 3, 1, 2).double().cpu(),
                    stride=stride, padding=pad)
     check(kp[0].permute(0, 3, 1, 2), ref)
