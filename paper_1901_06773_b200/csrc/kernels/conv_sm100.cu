@@ -1603,6 +1603,7 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   const bool padd = cfg.cm == 6;
   if (padd) {
     if (cfg.splits != 2 || cfg.bs || cfg.sk || a.scatter || a.stats || a.beta) return -1;
+    if (a.kb_total < 2) return -1;  // both slices must own k-blocks
     cfg.cm = 1;
   }
   if (c.mode == WGRAD) cfg.cm = 1;  // multicast of B across M-tiles: FWD / DGRAD only
