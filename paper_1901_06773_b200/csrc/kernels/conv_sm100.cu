@@ -1727,7 +1727,12 @@ Cfg tune(const Call& c, cudaStream_t st) {
   // 0: plain, 1: 2-CTA multicast, 3: 2-SM MMA pair.  (2, B-stationary, is
   // available through accudnn_conv_force_cfg but not tuned: measured no faster)
   // 5: split-K over a DSMEM-reduced CTA pair (2 slices)
+  static const int max_variant = [] {  // ACCUDNN_TUNE_VARIANTS: highest variant tried
+    const char* e = std::getenv("ACCUDNN_TUNE_VARIANTS");
+    return e ? std::atoi(e) : 6;
+  }();
   for (int variant : {0, 1, 3, 5, 6}) {
+   if (variant > max_variant) continue;
    const int cm = variant == 1 ? 2 : variant == 3 ? 4 : variant >= 5 ? variant : 1;
    const int bs = variant == 2 ? 1 : 0;
    if (variant > 0 && c.mode == WGRAD) continue;

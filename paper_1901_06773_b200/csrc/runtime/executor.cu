@@ -298,6 +298,13 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
           cq.size() == 1 && is_bn(net_.ops[static_cast<size_t>(cq[0])].kind))
         ok = false;
     }
+    // conv_bn_stats = 2: only the short layers (k*H*W <= 32768 rows), whose
+    // batch norms are latency-bound; a large layer's BN is bandwidth-bound
+    // and saves only one of its reads, less than the epilogue sums cost
+    if (cfg.conv_bn_stats == 2) {
+      const TensorShape& so = net_.shape[static_cast<size_t>(o)];
+      if (static_cast<long long>(cfg.k) * so.h * so.w > 16LL * 2048) ok = false;
+    }
     I.stats_ok[static_cast<size_t>(o)] = ok;
   }
   if (cfg.autotune) accudnn_conv_autotune(1);
