@@ -1823,7 +1823,9 @@ int run_call(const Call& c, cudaStream_t st) {
   std::copy(std::begin(c.key), std::end(c.key), key.begin());
   Cfg cfg;
   auto it = g_tuned.find(key);
-  if (it != g_tuned.end() && splits_ok(c, it->second.splits)) {
+  // (the 2-slice pair schedules, cm 5 / 6, need no split-K workspace)
+  if (it != g_tuned.end() &&
+      (it->second.cm >= 5 ? c.a.kb_total >= 2 : splits_ok(c, it->second.splits))) {
     cfg = it->second;
   } else {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
