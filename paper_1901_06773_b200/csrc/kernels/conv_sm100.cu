@@ -1389,7 +1389,11 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
     return static_cast<int>(cudaGetLastError());
   }
   const long long vec = static_cast<long long>(a.M) * (a.Ng / 4);
-  if (a.splits >= 16) {  // 8 lanes per output vector
+  static const int wide_from = [] {  // ACCUDNN_REDUCE_WIDE: slices from which 8 lanes share a vector
+    const char* e = std::getenv("ACCUDNN_REDUCE_WIDE");
+    return e ? std::atoi(e) : 16;
+  }();
+  if (a.splits >= wide_from) {  // 8 lanes per output vector
     const int wgrid = static_cast<int>(std::min<long long>((vec * 8 + 255) / 256, 16LL * sm_count()));
     launch_pdl(conv_splitk_reduce_wide_kernel, wgrid, 256, 0, st, a);
     return static_cast<int>(cudaGetLastError());

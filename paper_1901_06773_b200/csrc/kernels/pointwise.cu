@@ -672,8 +672,13 @@ int bn_launch(BnArgs a, cudaStream_t st) {
     const char* e = std::getenv("ACCUDNN_BN_L2HINTS");
     hints = e ? std::atoi(e) : 1;
   }
+  static double keep_mb[2] = {-1.0, -1.0};  // ACCUDNN_BN_KEEP_MB_FWD / _BWD overrides
+  if (keep_mb[MODE] < 0) {
+    const char* e = std::getenv(MODE == 1 ? "ACCUDNN_BN_KEEP_MB_BWD" : "ACCUDNN_BN_KEEP_MB_FWD");
+    keep_mb[MODE] = e ? std::atof(e) : (MODE == 1 ? 72.0 : 48.0);
+  }
   const double reread = 4.0 * static_cast<double>(a.M) * a.C * (MODE == 1 ? 2 : 1);
-  const bool fits = reread <= (MODE == 1 ? 72.0 : 48.0) * (1 << 20);
+  const bool fits = reread <= keep_mb[MODE] * (1 << 20);
   a.l2_keep = hints == 3 || ((hints == 1 || hints == 4) && fits);
   a.l2_last = hints == 3 || hints == 1 || (hints == 4 && fits);
   static int occ = 0;
