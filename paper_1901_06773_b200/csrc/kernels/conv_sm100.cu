@@ -103,9 +103,6 @@ struct Prob {
   unsigned* fix_cnt;   // per-tile arrival counters (zero between launches)
 };
 
-// epilogue TMEM reads pipelined one chunk ahead (ACCUDNN_EPI_PIPE=0: off)
-__constant__ int g_epi_pipe = 1;
-
 // experiment switch (ACCUDNN_CONV_DRAIN=1): epilogues wait for their bulk
 // stores' global writes before the CTA exits (default: only for the reads)
 __constant__ int g_conv_drain = 0;
@@ -741,22 +738,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* sk_blk = skp ? a.ws + (static_cast<long long>(tile) * a.sk_maxseg + split) * (kBM * BN)
                           : nullptr;
       const int nch = (ncols + 31) / 32;
-      // TMEM reads software-pipelined one chunk ahead: chunk ci + 1's
-      // tcgen05.ld is in flight while chunk ci is staged and stored
-      uint32_t nx[32];
-      if (nch > 0 && g_epi_pipe) ptx::tmem_ld32_issue(trow, nx);
 #pragma unroll 1
       for (int ci = 0; ci < nch; ++ci) {
         const int c0 = ci * 32;
         float cur[32];
-        if (g_epi_pipe) {
-          ptx::tmem_wait_ld_regs(nx);  // chunk ci landed (the only load in flight)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) cur[i] = __uint_as_float(nx[i]);
-          if (ci + 1 < nch) ptx::tmem_ld32_issue(trow + c0 + 32, nx);
-        } else {
-          ptx::tmem_ld32(trow + c0, cur);
-        }
+        ptx::tmem_ld32(trow + c0, cur);
         if (ci + 1 >= nch) {  // accumulator drained: release it to the MMA warp
           ptx::tc_fence_before();
           if constexpr (G == 2) {  // one arrive per warp on the even CTA's barrier
@@ -1799,10 +1785,6 @@ int run_call(const Call& c, cudaStream_t st) {
     const char* e = std::getenv("ACCUDNN_CONV_DRAIN");
     const int v = e ? std::atoi(e) : 0;
     if (v) cudaMemcpyToSymbol(g_conv_drain, &v, sizeof(v));
-    if (const char* p = std::getenv("ACCUDNN_EPI_PIPE")) {
-      const int w = std::atoi(p);
-      cudaMemcpyToSymbol(g_epi_pipe, &w, sizeof(w));
-    }
     return true;
   }();
   (void)drain_set;
