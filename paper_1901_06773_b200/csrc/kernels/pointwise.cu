@@ -92,6 +92,8 @@ struct BnArgs {
   float* dskip;          // SKIP, mode 1: gradient of the shortcut (+= when dskip_beta)
   int dskip_beta;
   int mask_smem;         // SKIP backward launched with the mask buffer (dynamic smem)
+  int row_cache;         // non-SKIP backward: phase 1 keeps its x / dy rows in dynamic
+                         // smem for phase 3 (short layers, <= kRowCache rows per thread)
   const float* stats_in; // mode 0: the producing conv's column sums [2][P][C] (P = ceil(M/32)):
                          // phase 1 sums these instead of reading x
   BnWs w;
@@ -161,6 +163,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* counters, unsigned nblock
 }
 
 constexpr int kBnPilotRows = 4;
+constexpr int kRowCache = 8;  // rows per thread the backward row cache holds (2 x 64 KB)
 __device__ __forceinline__ long long bn_pilot_row(long long M, int i) {
   return M * i / kBnPilotRows;
 }
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
   // is kept as 4 bits in shared memory (kMaskWords words per thread,
   // thread-interleaved), so phase 3 need not re-read the shortcut tensor
   extern __shared__ uint32_t mask_smem[];
+  float4* rcache = reinterpret_cast<float4*>(mask_smem);  // [row][x, dy][thread]
   constexpr int kMaskWords = 16;  // 128 rows per thread
   const long long first_row = r_begin + lane_r;
   const bool use_mask = MODE == 1 && SKIP && a.mask_smem &&
@@ -345,12 +349,22 @@ __global__ void __launch_bounds__(kBnThreads, (MODE == 0 || (CLUSTER && !SKIP)) 
       for (int u = 0; u < 4; ++u)
         keep_mask(kk + u,
                   consume(v[u], MODE == 1 ? d[u] : v[u], (MODE == 1 && SKIP) ? sk[u] : v[u]));
+      if (MODE == 1 && !SKIP && a.row_cache)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          rcache[(2 * (kk + u)) * kBnThreads + threadIdx.x] = v[u];
+          rcache[(2 * (kk + u) + 1) * kBnThreads + threadIdx.x] = d[u];
+        }
     }
     for (; r < r_end; r += step, ++kk) {
       const float4 v = ld_pol(a.x + r * C + c, p_keep);
       const float4 d = MODE == 1 ? ld_pol(a.dy + r * C + c, p_keep) : v;
       const float4 sk = (MODE == 1 && SKIP) ? ld_pol(a.skip + r * C + c, p_skip) : v;
       keep_mask(kk, consume(v, d, sk));
+      if (MODE == 1 && !SKIP && a.row_cache) {
+        rcache[(2 * kk) * kBnThreads + threadIdx.x] = v;
+        rcache[(2 * kk + 1) * kBnThreads + threadIdx.x] = d;
+      }
     }
   }
   if (MODE == 0 && c_ok && !a.stats_in && lane_r == 0)
@@ -624,6 +638,13 @@ __device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c
     const uint64_t p_last = l2_policy(a.l2_last ? 2 : 0);
     long long r = r_hi;  // reverse order, as above
     int kk = static_cast<int>((r_hi - first_row) / step);
+    if (!SKIP && a.row_cache) {  // the rows phase 1 kept in shared memory
+      const float4* rcache = reinterpret_cast<const float4*>(mask_smem);
+      for (; r >= r_begin; r -= step, --kk) {
+        const float4 xv = rcache[(2 * kk) * kBnThreads + threadIdx.x];
+        f(xv, rcache[(2 * kk + 1) * kBnThreads + threadIdx.x], xv, r, kk);
+      }
+    }
     for (; r - 3 * step >= r_begin; r -= 4 * step, kk -= 4) {
       float4 xv[4], dv[4], kv[4];
 #pragma unroll
@@ -651,6 +672,16 @@ __device__ __forceinline__ void bn_phase3(const BnArgs& a, bool c_ok, int lane_c
 //  * cooperative: Y row splits over the whole grid (all CTAs co-resident,
 //    2 per SM), partials in the workspace, one grid barrier; for the large
 //    early-stage layers that need every SM streaming.
+// ACCUDNN_BN_ROWCACHE=0: the backward re-reads its rows from L2 in phase 3
+inline bool row_cache_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ACCUDNN_BN_ROWCACHE");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // ACCUDNN_BN_RPB=0: plain ceil(M / Y) row splits (A/B switch)
 inline bool rpb_rounding() {
   static int v = -1;
@@ -780,6 +811,23 @@ int bn_launch(BnArgs a, cudaStream_t st) {
     }
   }
   a.Y = static_cast<int>(y);
+  // short backward layers: phase 1 keeps its rows in shared memory for phase 3
+  // (one CTA per SM in this mode, so 128 KB of dynamic smem is free)
+  if (MODE == 1 && !SKIP && row_cache_on()) {
+    const long long rpp = kBnThreads / l;
+    const long long rpb = a.rpb > 0 ? a.rpb : (a.M + y - 1) / y;
+    if ((rpb + rpp - 1) / rpp <= kRowCache) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        cudaFuncSetAttribute(bn_fused_kernel<MODE, false, SKIP>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(float4) * 2 * kRowCache * kBnThreads));
+        attr_set = true;
+      }
+      a.row_cache = 1;
+      cfg.dynamicSmemBytes = sizeof(float4) * 2 * kRowCache * kBnThreads;
+    }
+  }
   cfg.gridDim = dim3(gx, a.Y);
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
