@@ -1603,12 +1603,14 @@ int launch_cfg(const Call& c, Cfg cfg, cudaStream_t st) {
   }
   // cm 6: 2-slice split-K reduced by bulk reduce-adds into the zeroed output
   // (overwrite calls with row-major outputs only: with beta = 1 the old value
-  // would make the order matter)
-  const bool padd = cfg.cm == 6;
+  // would make the order matter); cm 7 / 8: the same over 2-SM MMA pairs
+  // (cm 2 / cm 4 tiles, each CTA of the pair reduce-adds its own 128 rows)
+  const bool padd = cfg.cm >= 6;
   if (padd) {
     if (cfg.splits != 2 || cfg.bs || cfg.sk || a.scatter || a.stats || a.beta) return -1;
     if (a.kb_total < 2) return -1;  // both slices must own k-blocks
-    cfg.cm = 1;
+    if (cfg.cm > 6 && c.mode == WGRAD) return -1;
+    cfg.cm = cfg.cm == 6 ? 1 : cfg.cm == 7 ? 2 : 4;
   }
   if (c.mode == WGRAD) cfg.cm = 1;  // multicast of B across M-tiles: FWD / DGRAD only
   if (cfg.bs && (c.mode == WGRAD || cfg.splits != 1 || cfg.cm != 1 ||
@@ -1730,12 +1732,13 @@ Cfg tune(const Call& c, cudaStream_t st) {
   float best_ms = 1e30f;
   // 0: plain, 1: 2-CTA multicast, 3: 2-SM MMA pair.  (2, B-stationary, is
   // available through accudnn_conv_force_cfg but not tuned: measured no faster)
-  // 5: split-K over a DSMEM-reduced CTA pair (2 slices)
+  // 5: split-K over a DSMEM-reduced CTA pair (2 slices); 6 / 7 / 8: 2 slices reduce-added
+  // into the zeroed output by single CTAs / 2-SM pairs / multicast pairs
   static const int max_variant = [] {  // ACCUDNN_TUNE_VARIANTS: highest variant tried
     const char* e = std::getenv("ACCUDNN_TUNE_VARIANTS");
-    return e ? std::atoi(e) : 6;
+    return e ? std::atoi(e) : 8;
   }();
-  for (int variant : {0, 1, 3, 5, 6}) {
+  for (int variant : {0, 1, 3, 5, 6, 7, 8}) {
    if (variant > max_variant) continue;
    const int cm = variant == 1 ? 2 : variant == 3 ? 4 : variant >= 5 ? variant : 1;
    const int bs = variant == 2 ? 1 : 0;
@@ -1805,7 +1808,7 @@ int run_call(const Call& c, cudaStream_t st) {
       f.bs = 1;
       f.splits = 1;
     }
-    if (g_force.cm == 6) {  // test hook: 2-slice split-K by reduce-adds into the zeroed output
+    if (g_force.cm >= 6) {  // test hook: 2-slice split-K by reduce-adds into the zeroed output
       f.splits = 2;
       f.bs = 0;
       f.sk = 0;
@@ -2116,7 +2119,7 @@ extern "C" int accudnn_conv_tune_import(const char* text) {
     for (int& v : key) ok = ok && static_cast<bool>(ls >> v);
     ok = ok && static_cast<bool>(ls >> cfg.bn >> cfg.splits);
     if (!ok) continue;
-    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4 && cfg.cm != 5 && cfg.cm != 6))
+    if (!(ls >> cfg.cm) || (cfg.cm != 1 && cfg.cm != 2 && cfg.cm != 4 && (cfg.cm < 5 || cfg.cm > 8)))
       cfg.cm = 1;
     if (!(ls >> cfg.bs) || (cfg.bs != 0 && cfg.bs != 1)) cfg.bs = 0;
     if (!(ls >> cfg.sk) || (cfg.sk != 0 && cfg.sk != 1)) cfg.sk = 0;

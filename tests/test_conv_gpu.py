@@ -66,7 +66,7 @@ def check(got, ref):
 @pytest.fixture(params=["tma", "tma_cluster2", "tma_pair", "tma_pair_bn256_split2", "tma_pair_bn64",
                         "tma_bn64_split3", "tma_bstat", "tma_streamk", "tma_streamk_bn64",
                         "tma_kpair", "tma_kpair_bn256", "tma_kpair_bn64", "tma_padd", "tma_padd_bn256",
-                        "cpasync"])
+                        "tma_padd_cluster2", "tma_padd_pair", "cpasync"])
 def impl(request):
     """TMA kernel with the analytic config, with the B tile multicast across an
     M-tile pair (cluster of 2), as a CTA pair running 2-SM MMAs (256-row
@@ -100,6 +100,10 @@ def impl(request):
         lib.accudnn_conv_force_cfg(0, 0, 6)
     elif request.param == "tma_padd_bn256":
         lib.accudnn_conv_force_cfg(256, 0, 6)
+    elif request.param == "tma_padd_cluster2":  # the same over multicast M-tile pairs
+        lib.accudnn_conv_force_cfg(0, 0, 7)
+    elif request.param == "tma_padd_pair":  # the same over 2-SM MMA pairs
+        lib.accudnn_conv_force_cfg(0, 0, 8)
     yield request.param
     lib.accudnn_conv_force_cfg(0, 0, 0)
     lib.accudnn_set_conv_impl(1)
@@ -386,6 +390,20 @@ def test_kpair_equals_two_slice_workspace_reduction(cuda_dev, shape, bn):
         assert torch.equal(pa[i], pa2[i])
     for i in (1, 3):
         assert rel_err(pa[i].double(), ws[i].double()) < 1e-5
+    # cm 7 / 8: the reduce-adds over CTA pairs (multicast / 2-SM MMA) equal the
+    # same pairs' 2-slice workspace reduction (cm 2 / 4, splits 2)
+    for cm_ws, cm_pa in ((2, 7), (4, 8)):
+        lib.accudnn_conv_set_workspace(None, ctypes.c_ulonglong(512 << 20))
+        try:
+            wsp = run(cm_ws)
+        finally:
+            lib.accudnn_conv_set_workspace(None, ctypes.c_ulonglong(64 << 20))
+        pp, pp2 = run(cm_pa), run(cm_pa)
+        for i in (0, 2):
+            assert torch.equal(wsp[i], pp[i]), (cm_pa, i)
+            assert torch.equal(pp[i], pp2[i])
+        for i in (1, 3):
+            assert rel_err(pp[i].double(), wsp[i].double()) < 1e-5
     ref = F.conv2d(x_d.permute(0, 3, 1, 2).double().cpu(), w_d.permute(0, 3, 1, 2).double().cpu(),
                    stride=stride, padding=pad)
     check(kp[0].permute(0, 3, 1, 2), ref)

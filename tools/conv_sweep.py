@@ -37,8 +37,8 @@ fn = {"fwd": lambda s=None: lib.accudnn_conv_fwd(ctypes.byref(d), x.data_ptr(), 
 ms = timeit(fn, graph=True)
 print(f"tuned: {ms*1e3:.1f} us {flops/ms/1e9:.0f} TF/s", flush=True)
 for bn in (64, 128, 256):
-    for cm in (1, 2, 4, 5, 6):
-        for sp in (1, 2, 3, 4, 6, 8):
+    for cm in (1, 2, 4, 5, 6, 7, 8):
+        for sp in ((1, 2, 3, 4, 6, 8) if cm < 5 else (2,)):
             lib.accudnn_conv_force_cfg(bn, sp, cm)
             try:
                 ms = timeit(fn, graph=True)
