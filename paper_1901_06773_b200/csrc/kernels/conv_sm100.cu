@@ -1723,11 +1723,58 @@ Cfg model_cfg(const Call& c) {
 // once and then timed (min of 3, CUDA events on the caller's stream), never
 // during stream capture; accumulating (beta = 1) calls are tuned on a scratch
 // output.  The result is cached per shape for the life of the process.
+// Seconds per launch of a candidate as the captured step runs it: a CUDA graph
+// of kTuneReps back-to-back launches on the tuning stream, best of two
+// replays.  (Timed eagerly, the host launch gaps and the pair-add memset's
+// own launch would be charged to every candidate; the step pays neither.)
+constexpr int kTuneReps = 4;
+float time_in_graph(const Call& c, const Cfg& cand, cudaStream_t ts, cudaEvent_t e0,
+                    cudaEvent_t e1) {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  if (cudaStreamBeginCapture(ts, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return 1e30f;
+  }
+  bool ok = true;
+  for (int i = 0; i < kTuneReps && ok; ++i) ok = launch_cfg(c, cand, ts) == 0;
+  const cudaError_t ec = cudaStreamEndCapture(ts, &g);
+  float best = 1e30f;
+  if (ok && ec == cudaSuccess && g && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess) {
+    cudaGraphLaunch(ge, ts);  // warm: tensor maps, L2
+    for (int r = 0; r < 2; ++r) {
+      cudaEventRecord(e0, ts);
+      cudaGraphLaunch(ge, ts);
+      cudaEventRecord(e1, ts);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = std::min(best, ms / kTuneReps);
+    }
+  }
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  return best;
+}
+
 Cfg tune(const Call& c, cudaStream_t st) {
   static const int kSplits[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64, 96, 128};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  // candidates run on a private stream ordered after the caller's work (the
+  // caller's stream may be the legacy stream, which cannot be captured); the
+  // caller's stream waits for them at the end (same workspace)
+  static cudaStream_t ts = [] {
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    return s;
+  }();
+  cudaEvent_t dep;
+  cudaEventCreateWithFlags(&dep, cudaEventDisableTiming);
+  cudaEventRecord(dep, st);
+  cudaStreamWaitEvent(ts, dep, 0);
   Cfg best = model_cfg(c);
   float best_ms = 1e30f;
   // 0: plain, 1: 2-CTA multicast, 3: 2-SM MMA pair.  (2, B-stationary, is
@@ -1754,20 +1801,11 @@ Cfg tune(const Call& c, cudaStream_t st) {
       if (!splits_ok(c, s)) continue;
       if (bs && s != 1) continue;
       const Cfg cand{bn, s, cm, bs, sk};
-      if (launch_cfg(c, cand, st) != 0) {
+      if (launch_cfg(c, cand, ts) != 0) {
         cudaGetLastError();
         continue;
       }
-      float t = 1e30f;
-      for (int r = 0; r < 3; ++r) {
-        cudaEventRecord(e0, st);
-        launch_cfg(c, cand, st);
-        cudaEventRecord(e1, st);
-        cudaEventSynchronize(e1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        t = std::min(t, ms);
-      }
+      const float t = time_in_graph(c, cand, ts, e0, e1);
       if (t < best_ms) {
         best_ms = t;
         best = cand;
@@ -1776,6 +1814,9 @@ Cfg tune(const Call& c, cudaStream_t st) {
     }
    }
   }
+  cudaEventRecord(dep, ts);
+  cudaStreamWaitEvent(st, dep, 0);
+  cudaEventDestroy(dep);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return best;
