@@ -1728,6 +1728,13 @@ Cfg model_cfg(const Call& c) {
 // replays.  (Timed eagerly, the host launch gaps and the pair-add memset's
 // own launch would be charged to every candidate; the step pays neither.)
 constexpr int kTuneReps = 4;
+bool tune_eager() {  // ACCUDNN_TUNE_EAGER=1: time candidates as eager single launches
+  static const bool v = [] {
+    const char* e = std::getenv("ACCUDNN_TUNE_EAGER");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
 float time_in_graph(const Call& c, const Cfg& cand, cudaStream_t ts, cudaEvent_t e0,
                     cudaEvent_t e1) {
   cudaGraph_t g = nullptr;
@@ -1805,7 +1812,20 @@ Cfg tune(const Call& c, cudaStream_t st) {
         cudaGetLastError();
         continue;
       }
-      const float t = time_in_graph(c, cand, ts, e0, e1);
+      float t = 1e30f;
+      if (tune_eager()) {  // A/B: eager single launches (the round-1 tuner)
+        for (int r = 0; r < 3; ++r) {
+          cudaEventRecord(e0, ts);
+          launch_cfg(c, cand, ts);
+          cudaEventRecord(e1, ts);
+          cudaEventSynchronize(e1);
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, e0, e1);
+          t = std::min(t, ms);
+        }
+      } else {
+        t = time_in_graph(c, cand, ts, e0, e1);
+      }
       if (t < best_ms) {
         best_ms = t;
         best = cand;
