@@ -305,6 +305,12 @@ Executor::Executor(const ExecConfig& cfg, const std::vector<char>& swapped)
       const TensorShape& so = net_.shape[static_cast<size_t>(o)];
       if (static_cast<long long>(cfg.k) * so.h * so.w > 16LL * 2048) ok = false;
     }
+    // conv_bn_stats = 3 (A/B): only the layers whose output exceeds 64 MB,
+    // where the BN's second read of x comes from HBM
+    if (cfg.conv_bn_stats == 3) {
+      const TensorShape& so = net_.shape[static_cast<size_t>(o)];
+      if (4LL * cfg.k * so.h * so.w * so.c <= (64LL << 20)) ok = false;
+    }
     I.stats_ok[static_cast<size_t>(o)] = ok;
   }
   if (cfg.autotune) accudnn_conv_autotune(1);
