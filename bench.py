@@ -348,8 +348,22 @@ def reference_cpu_path(network_json, hardware_json, model_json, k_ours=None, pla
            "modelled_iter_ms": None if summ.get("oom") else round(summ["iter_time_s"] * 1e3, 3),
            "modelled_images_per_s": None if summ.get("oom") else round(k / summ["iter_time_s"], 2),
            "modelled_stall_ms": None if summ.get("oom") else round(summ["total_stall_s"] * 1e3, 4)}
+    # the reference's parallel grid sweep (sweep.cpp, OpenMP over cells on all
+    # host cores; the bench/sweep_bench.cpp:46-64 method) on the same documents
+    ks = sorted({8, 16, 32, k})
+    t0 = time.perf_counter()
+    sw_ref = planner.sweep(network_json, hardware_json, model_json, ks, "naive,dynamic,resident",
+                           parallel=True, **R)
+    out["sweep_seconds_parallel"] = round(time.perf_counter() - t0, 4)
+    out["sweep_cells"] = 3 * len(ks)
+    out["sweep_threads"] = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     if plan_ours is not None:
         out["plan_parity"] = plan_ref == plan_ours
+        # the same grid through the B200 host library: identical CSV
+        t0 = time.perf_counter()
+        sw = planner.sweep(network_json, hardware_json, model_json, ks, "naive,dynamic,resident")
+        out["sweep_seconds_b200_host"] = round(time.perf_counter() - t0, 4)
+        out["sweep_parity"] = sw == sw_ref
     return out
 
 
