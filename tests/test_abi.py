@@ -38,3 +38,21 @@ def test_no_cpu_fallback_symbols():
     lib = _native.cuda_lib()
     for suffix in ("cpu", "reference", "fallback"):
         assert not hasattr(lib, f"accudnn_conv_fwd_{suffix}")
+
+
+def test_committed_conv_tune_table_round_trips():
+    """profiles/b200/conv_tune.txt (the B200-tuned kernel configurations every
+    bench / test run imports) parses completely -- a line the parser rejected
+    would silently fall back to run-time tuning -- holds every shape of the
+    headline step (k = 42: fwd / dgrad / wgrad of the ResNet-152 convs), and
+    exports back unchanged.  Host-only code: no GPU needed."""
+    text = open(os.path.join(ROOT, "profiles", "b200", "conv_tune.txt")).read()
+    lines = sorted(l.strip() for l in text.splitlines() if l.strip())
+    for l in lines:
+        v = [int(t) for t in l.split()]
+        assert len(v) in (18, 19), l
+        bn, splits, cm = v[14], v[15], v[16]
+        assert bn in (64, 128, 256) and splits >= 1 and cm in (1, 2, 4, 5, 6, 7, 8), l
+    assert sum(1 for l in lines if l.split()[1] == "42") >= 70
+    _native.conv_tune_import(text)
+    assert sorted(_native.conv_tune_export().splitlines()) == lines
