@@ -29,6 +29,7 @@ if os.path.exists(tune):
 
 CASES = [  # arch, image, classes, cap GiB, k, pins
     ("resnet20", 32, 12, 8, 8, "plan"),
+    ("resnet20", 32, 12, 8, 8, "naive"),   # config 1's naive-mode run
     ("resnet1001", 32, 12, 8, 41, "naive"),
     ("resnet1001", 32, 12, 8, 41, "every3"),
     ("resnet152", 224, 1000, 8, 8, "naive"),
